@@ -1,0 +1,426 @@
+"""Benchmark of the PAT decode-attention hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl pat|reference]
+
+One step = one decode-attention layer (pack plan reused -- lazy update -- then
+forward + merge) over synthetic bf16 Q / paged K,V of the named BASELINE.json
+workload (default configs[1] = c2, the two-level prefix tree, Llama-3-8B
+attention shape).  Inputs are resident in HBM; L2 (126 MB) is flushed before
+every timed step by writing a 512 MB buffer.  value = unique KV bytes
+(theoretical_min_kv_bytes, simulator.py:78-82) of all ranks / max-over-ranks
+layer time.  N > 1: the KV heads are sharded across ranks (no collective on the
+path), strong scaling of the same layer.
+
+``--impl reference`` times the reference algorithm on the host CPU (the oracle
+port of prefixpack.run_packed_attention, float64 numpy, one process per core).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "decode attn latency µs/layer + achieved HBM GB/s (unique KV) vs roofline, 1/2/4/8 GPU"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return dict(PEAKS_FALLBACK)
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampler running during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception as exc:  # pragma: no cover - no NVML
+            self.nv = None
+            self.err = str(exc)
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU reference arm / baseline (oracle port of prefixpack.run_packed_attention)
+# ------------------------------------------------------------------------------------------
+
+_CPU_STATE = {}
+
+
+def _cpu_worker(args):
+    from oracle import attn_oracle as AO
+
+    idx_list = args
+    q, store, units = _CPU_STATE["q"], _CPU_STATE["store"], _CPU_STATE["units"]
+    res = []
+    for i in idx_list:
+        qs, blocks, n = units[i]
+        k, v = AO.span_kv(store, blocks, n)
+        res.append((i, AO.partial(q[np.asarray(qs)], k, v)))
+    return res
+
+
+def cpu_reference(config: str, kv_heads_sample: int, steps: int, warmup: int, procs: int):
+    """Time the reference pipeline (packs -> reference split_long_kv -> per-unit
+    cta_partial in float64 -> online-softmax fold in unit order) on the host.
+    Sample: ``kv_heads_sample`` of the config's kv heads (with their query heads),
+    all queries and all tokens.  Returns (GB/s on the sample's unique bytes, sec/step)."""
+    import multiprocessing as mp
+
+    from oracle import attn_oracle as AO
+    from oracle import pack_oracle as PO
+    from paper_2511_22333_b200 import configs
+
+    w = configs.workload(config)
+    G = w.num_heads // w.num_kv_heads
+    kvh = kv_heads_sample
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((w.batch, kvh * G, w.head_dim))
+    blocks = sorted({b for r in w.rows for b in r})
+    store = {b: (rng.standard_normal((w.block_size, kvh, w.head_dim)),
+                 rng.standard_normal((w.block_size, kvh, w.head_dim))) for b in blocks}
+    packs = PO.pack_batch(w.rows, w.valid_last, w.block_size)
+    units = [(t[0], t[1], t[2]) for t in PO.split_long_kv([(p[0], p[1], p[2]) for p in packs], w.block_size)]
+    _CPU_STATE.update(q=q, store=store, units=units)
+    order = sorted(range(len(units)), key=lambda i: -len(units[i][0]) * units[i][2])
+    chunks = [order[i::procs] for i in range(procs)]
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(procs) as pool:
+        for it in range(warmup + steps):
+            t0 = time.perf_counter()
+            parts = {}
+            for res in pool.map(_cpu_worker, chunks):
+                parts.update(dict(res))
+            M = np.full((w.batch, kvh * G), -np.inf)
+            L = np.zeros((w.batch, kvh * G))
+            O = np.zeros((w.batch, kvh * G, w.head_dim))
+            for i, (qs, _, _) in enumerate(units):
+                AO.fold((M, L, O), np.asarray(qs), *parts[i])
+            out = O / L[:, :, None]
+            dt = time.perf_counter() - t0
+            if it >= warmup:
+                times.append(dt)
+    assert np.isfinite(out).all()
+    sample_bytes = w.distinct_tokens() * kvh * w.head_dim * 2 * 2
+    sec = float(np.mean(times))
+    return sample_bytes / sec / 1e9, sec, sample_bytes
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2511_22333_b200 import configs
+
+    w = configs.workload(args.config)
+    procs = os.cpu_count() or 1
+    kvh = 2
+    gbs, sec, nbytes = cpu_reference(args.config, kvh, args.steps, args.warmup, procs)
+    sample = (f"{args.config}: all {w.batch} queries x all tokens, {kvh} of {w.num_kv_heads} kv heads "
+              f"({kvh * w.num_heads // w.num_kv_heads} q heads); packs + reference split_long_kv; float64")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 6), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded normal)",
+        "config": {"workload": args.config, "description": w.description, "sample_bytes": nbytes},
+        "cpu_baseline": {"value": round(gbs, 6), "unit": "GB/s", "cores": procs, "kind": "port", "sample": sample},
+        "e2e": {"value": round(gbs, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+
+def shard_heads(w, rank, world):
+    if w.num_kv_heads % world:
+        raise SystemExit(f"{world} ranks do not divide {w.num_kv_heads} kv heads")
+    kvh = w.num_kv_heads // world
+    return kvh, kvh * (w.num_heads // w.num_kv_heads)
+
+
+def measure_config(name, rank, world, steps, warmup, dev, flush, split="native", dtype_name="bfloat16",
+                   with_e2e=False, sampler=None):
+    import torch
+
+    import paper_2511_22333_b200 as P
+    from paper_2511_22333_b200 import configs
+
+    dtype = getattr(torch, dtype_name)
+    w = configs.workload(name)
+    kvh, hq = shard_heads(w, rank, world)
+    table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    # packer: host C++ plan build (cold), reported separately (lazy update amortises it)
+    t0 = time.perf_counter()
+    plan = P.PatPlan.from_table(table, hq, kvh, w.head_dim, split=split)
+    pack_ms = (time.perf_counter() - t0) * 1e3
+    info = plan.info()
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    nb = w.num_pool_blocks()
+    kc = torch.randn(nb, w.block_size, kvh, w.head_dim, device=dev, dtype=dtype, generator=g)
+    vc = torch.randn(nb, w.block_size, kvh, w.head_dim, device=dev, dtype=dtype, generator=g)
+    q = torch.randn(w.batch, hq, w.head_dim, device=dev, dtype=dtype, generator=g)
+    out = torch.empty_like(q)
+    ws = torch.empty(max(plan.workspace_bytes(), 256), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def layer():
+        P.pat_attention(plan, q, kc, vc, out=out, workspace=ws)
+
+    for _ in range(warmup):
+        flush.zero_()
+        layer()
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    ctx = sampler if sampler is not None else _Null()
+    with ctx:
+        for i in range(steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            layer()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    per = [a.elapsed_time(b) for a, b in evs]
+    t_ms = float(np.mean(per))
+    unique = info.unique_tokens * kvh * w.head_dim * 2 * 2
+    res = {"name": name, "t_ms": t_ms, "t_min_ms": float(np.min(per)), "unique_bytes": unique,
+           "pack_ms": pack_ms, "info": info, "launches_per_step": _launches(plan), "kvh": kvh, "hq": hq}
+    if with_e2e:
+        res["e2e"] = measure_e2e(P, plan, w, table, q, kc, vc, ws, steps, warmup, dev, flush)
+    plan.close()
+    del kc, vc
+    torch.cuda.empty_cache()
+    return res
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def _launches(plan):
+    """Kernels per layer: one forward kernel per non-empty variant + the merge."""
+    return plan.info().n_launches
+
+
+def measure_e2e(P, plan, w, table, q, kc, vc, ws, steps, warmup, dev, flush):
+    """End to end through the public API with HOST buffers: per step H2D of Q and of
+    the block table + seq lens (pinned), the layer, D2H of the output."""
+    import torch
+
+    qh = q.cpu().pin_memory()
+    bt, sl = table.padded()
+    bth = torch.from_numpy(bt).pin_memory()
+    slh = torch.from_numpy(sl).pin_memory()
+    qd = torch.empty_like(q)
+    btd = torch.empty(bt.shape, dtype=torch.int32, device=dev)
+    sld = torch.empty(sl.shape, dtype=torch.int32, device=dev)
+    outh = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+    outd = torch.empty_like(q)
+    stream = torch.cuda.current_stream(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+
+    def step(i=None):
+        if i is not None:
+            evs[i][0].record(stream)
+        qd.copy_(qh, non_blocking=True)
+        btd.copy_(bth, non_blocking=True)
+        sld.copy_(slh, non_blocking=True)
+        P.pat_attention(plan, qd, kc, vc, out=outd, workspace=ws)
+        outh.copy_(outd, non_blocking=True)
+        if i is not None:
+            evs[i][1].record(stream)
+
+    for _ in range(warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+    for i in range(steps):
+        flush.zero_()
+        step(i)
+    torch.cuda.synchronize(dev)
+    per = [a.elapsed_time(b) for a, b in evs]
+    h2d = qh.numel() * qh.element_size() + bth.numel() * 4 + slh.numel() * 4
+    d2h = outh.numel() * outh.element_size()
+    return {"t_ms": float(np.mean(per)), "h2d": h2d, "d2h": d2h}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="pat", choices=["pat", "reference"])
+    ap.add_argument("--split", default="native", choices=["native", "reference", "none"])
+    ap.add_argument("--no-others", action="store_true", help="skip the other configs' latency table")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=dev)
+    assert args.warmup >= 3, "warm-up must be >= 3 steps"
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    peaks = load_peaks()
+
+    sampler = ClockSampler(local)
+    main_res = measure_config(args.config, rank, world, args.steps, args.warmup, dev, flush, split=args.split,
+                              with_e2e=True, sampler=sampler)
+    others = {}
+    if not args.no_others:
+        for name in ("c1", "c2", "c3", "c4", "c5"):
+            if name == args.config:
+                continue
+            r = measure_config(name, rank, world, max(10, args.steps // 2), args.warmup, dev, flush,
+                               split=args.split)
+            others[name] = r
+
+    # max over ranks of the per-layer time; bytes summed over ranks
+    def reduce_max(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def reduce_sum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t)
+        return float(t.item())
+
+    t_ms = reduce_max(main_res["t_ms"])
+    tot_bytes = reduce_sum(main_res["unique_bytes"])
+    e2e_ms = reduce_max(main_res["e2e"]["t_ms"])
+    other_summary = {}
+    for name, r in others.items():
+        tm = reduce_max(r["t_ms"])
+        tb = reduce_sum(r["unique_bytes"])
+        other_summary[name] = {"us_per_layer": round(tm * 1e3, 2), "GB/s": round(tb / (tm * 1e-3) / 1e9, 1),
+                               "frac_of_measured_hbm": round(tb / (tm * 1e-3) / 1e9 / peaks["hbm_gbs"], 3),
+                               "packs": r["info"].n_packs, "items": r["info"].n_items}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            gbs, sec, nbytes = cpu_reference(args.config, 1, 1, 0, 1)
+            cpu = {"value": round(gbs, 6), "unit": "GB/s", "cores": 1, "kind": "port",
+                   "sample": f"{args.config}: all queries x all tokens, 1 of 8 kv heads, float64 numpy "
+                             f"(oracle port of run_packed_attention), {sec:.2f} s"}
+        except Exception as exc:  # keep the GPU line even if the CPU leg fails
+            cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        gbs = tot_bytes / (t_ms * 1e-3) / 1e9
+        info = main_res["info"]
+        clocks = sampler.summary()
+        line = {
+            "metric": METRIC, "value": round(gbs, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_ms, 5), "latency_us_per_layer": round(t_ms * 1e3, 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded torch.randn Q/K/V; BASELINE.json block-table structure)",
+            "config": {"workload": args.config, "description": configs_desc(args.config),
+                       "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+                       "split": args.split, "l2": "flushed before every step (512 MB write)",
+                       "unique_kv_bytes": int(tot_bytes), "packs": info.n_packs, "units": info.n_units,
+                       "work_items": info.n_items, "merge_queries": info.n_merge_q},
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": None,
+                         "kernel": "one layer: pat forward kernels (all variants, multi-stream) + merge",
+                         "peak_source": peaks["source"]},
+            "e2e": {"value": round(tot_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": main_res["e2e"]["h2d"], "d2h_bytes_per_step": main_res["e2e"]["d2h"],
+                    "us_per_layer": round(e2e_ms * 1e3, 2)},
+            "gpu_launches": main_res["launches_per_step"] * args.steps,
+            "packer_ms_host_cold": round(main_res["pack_ms"], 3),
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "all_configs": other_summary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def configs_desc(name):
+    from paper_2511_22333_b200 import configs
+
+    return configs.workload(name).description
+
+
+if __name__ == "__main__":
+    sys.exit(main())

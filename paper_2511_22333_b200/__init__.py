@@ -1,0 +1,22 @@
+"""B200-native PAT decode attention: pack -> multi-tile forward -> merge.
+
+Drop-in for the hot path of the reference ``prefixpack`` package
+(``/root/reference/pkg/src/prefixpack/__init__.py:10-86``): the same public
+names for the pack stage, the forward/merge entry point and the domain types;
+the work runs in libpatb200.so (``include/pat.h``) -- a host C++ / CUDA packer
+and hand-written sm_100a kernels.  The reference's analytical cost model,
+simulator and CLI are out of scope.
+"""
+
+from .errors import (CoverageGap, EmptyFeasibleSet, EmptyPartialList, EmptySpan, InvalidChildIndex,
+                     InvalidSpec, MissingRegisterEntry, NativeError, NoFeasibleConfig, NonPositiveDenominator,
+                     PrefixpackError, ShapeMismatch)
+from .workload import (BlockTable, CtaPack, Partition, WorkloadSpec, assemble_partition, generate_workload,
+                       validate_partition)
+from .packer import (CtaTask, PackCache, baseline_query_centric, naive_per_node, pack_batch, pack_batch_async,
+                     split_long_kv)
+from .plan import PatPlan
+from .attention import PatDecoder, kv_pool_from_store, pat_attention, run_packed_attention
+from .metrics import distinct_block_census, theoretical_min_kv_bytes
+
+__version__ = "0.1.0"

@@ -1,0 +1,144 @@
+"""Forward + merge of the drop-in surface.
+
+* ``run_packed_attention`` -- same signature and semantics as the reference
+  (``attention.py:202-239``): any Partition / [CtaTask] / [CtaPack], a
+  ``{block_id: (K, V)}`` store and numpy Q in; numpy [B, H, d] out.  Inputs are
+  rounded to fp16 (or bf16) and the attention runs in libpatb200 on the GPU.
+* ``pat_attention`` / ``PatDecoder`` -- the tensor API a serving engine calls:
+  Q [B, H, d], paged caches [num_blocks, page, KVH, d] (vLLM NHD layout), block
+  tables + seq lens; lazy plan reuse keyed by the table fingerprint
+  (``packer.py:189-221``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence, Union
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import CoverageGap, ShapeMismatch
+from .packer import CtaTask, PackCache
+from .plan import PatPlan
+from .workload import BlockTable, CtaPack, Partition, WorkloadSpec
+
+_DTYPES = {torch.float16: N.PAT_DTYPE_F16, torch.bfloat16: N.PAT_DTYPE_BF16}
+
+
+def _coverage_units(parts) -> list:
+    items = parts.packs if isinstance(parts, Partition) else list(parts)
+    units = []
+    for it in items:
+        if isinstance(it, CtaTask) or type(it).__name__ == "CtaTask":
+            units.append((tuple(it.queries), tuple(it.block_ids), int(it.kv_len)))
+        elif isinstance(it, CtaPack) or type(it).__name__ == "CtaPack":
+            units.append((tuple(it.query_ids), tuple(it.block_ids), int(it.kv_len)))
+        else:
+            raise TypeError(f"cannot interpret {type(it)!r} as a coverage unit")
+    return units
+
+
+def pat_attention(plan: PatPlan, q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
+                  out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                  scale: Optional[float] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """One decode-attention layer through ``pat_forward`` (stream-ordered, no sync)."""
+    if q.dtype not in _DTYPES or k_cache.dtype != q.dtype or v_cache.dtype != q.dtype:
+        raise ShapeMismatch("q, k_cache, v_cache must share dtype float16 or bfloat16")
+    if q.dim() != 3 or q.shape[1] != plan.num_heads or q.shape[2] != plan.head_dim:
+        raise ShapeMismatch(f"q must be [B, {plan.num_heads}, {plan.head_dim}], got {tuple(q.shape)}")
+    if k_cache.shape != v_cache.shape or k_cache.dim() != 4 or k_cache.shape[2] != plan.num_kv_heads \
+            or k_cache.shape[3] != plan.head_dim:
+        raise ShapeMismatch("k_cache/v_cache must be [num_blocks, page, KVH, d]")
+    if not (q.is_cuda and k_cache.is_cuda and v_cache.is_cuda):
+        raise ShapeMismatch("tensors must be on a CUDA device")
+    if not (q.is_contiguous() and k_cache.is_contiguous() and v_cache.is_contiguous()):
+        raise ShapeMismatch("tensors must be contiguous")
+    if out is None:
+        out = torch.empty_like(q)
+    need = plan.workspace_bytes()
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=q.device)
+    s = stream if stream is not None else torch.cuda.current_stream(q.device)
+    st = N.lib().pat_forward(plan.handle, C.c_void_p(q.data_ptr()), C.c_void_p(k_cache.data_ptr()),
+                             C.c_void_p(v_cache.data_ptr()), k_cache.shape[0], C.c_void_p(out.data_ptr()),
+                             C.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size(),
+                             _DTYPES[q.dtype], float(scale) if scale else 0.0, C.c_void_p(s.cuda_stream))
+    N.check(st, "pat_forward")
+    return out
+
+
+class PatDecoder:
+    """Serving-side helper: plan cache (lazy update) + reusable workspace."""
+
+    def __init__(self, num_heads: int, num_kv_heads: int, head_dim: int, split: str = "native",
+                 device: Union[str, torch.device] = "cuda"):
+        self.num_heads, self.num_kv_heads, self.head_dim = num_heads, num_kv_heads, head_dim
+        self.split = split
+        self.device = torch.device(device)
+        self.cache = PackCache()
+        self._ws: Optional[torch.Tensor] = None
+
+    def plan_for(self, table: BlockTable) -> PatPlan:
+        fp = table.fingerprint()
+        plan = self.cache.lookup(fp)
+        if plan is None:
+            plan = PatPlan.from_table(table, self.num_heads, self.num_kv_heads, self.head_dim, split=self.split)
+            self.cache.store(fp, plan)
+        return plan
+
+    def workspace(self, plan: PatPlan) -> torch.Tensor:
+        need = max(plan.workspace_bytes(), 256)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def __call__(self, table: BlockTable, q, k_cache, v_cache, out=None, scale=None):
+        plan = self.plan_for(table)
+        return pat_attention(plan, q, k_cache, v_cache, out=out, workspace=self.workspace(plan), scale=scale)
+
+
+def kv_pool_from_store(kv_store: dict, block_size: int, dtype=torch.float16, device="cuda"):
+    """Paged caches [max_id + 1, page, KVH, d] from the reference ``{id: (K, V)}`` store."""
+    ids = sorted(kv_store)
+    k0 = np.asarray(kv_store[ids[0]][0])
+    nb = ids[-1] + 1
+    kh = np.zeros((nb,) + k0.shape, dtype=np.float32)
+    vh = np.zeros((nb,) + k0.shape, dtype=np.float32)
+    for b in ids:
+        kh[b] = kv_store[b][0]
+        vh[b] = kv_store[b][1]
+    if kh.shape[1] != block_size:
+        raise ShapeMismatch(f"store blocks hold {kh.shape[1]} tokens, table block_size is {block_size}")
+    return (torch.from_numpy(kh).to(device=device, dtype=dtype), torch.from_numpy(vh).to(device=device, dtype=dtype))
+
+
+def run_packed_attention(table: BlockTable, partition_or_tasks: Union[Partition, Sequence[CtaTask], Sequence[CtaPack]],
+                         kv_store: dict, q: np.ndarray, spec: WorkloadSpec, intermediate_dtype=None,
+                         *, dtype: torch.dtype = torch.float16, split: str = "none",
+                         device: Union[str, torch.device] = "cuda") -> np.ndarray:
+    """Drop-in for ``prefixpack.run_packed_attention`` (``attention.py:202-239``).
+
+    Coverage is checked natively (``CoverageGap``); partials are always fp32 on
+    the device, so ``intermediate_dtype`` is accepted and has no further effect.
+    Returns float64 [B, H, d] like the reference (computed from ``dtype`` inputs)."""
+    del intermediate_dtype
+    units = _coverage_units(partition_or_tasks)
+    q = np.asarray(q)
+    if q.ndim != 3 or q.shape[0] != table.num_queries:
+        raise ShapeMismatch("Q row count must match the table")
+    if table.num_queries == 0:
+        return np.zeros(q.shape, dtype=np.float64)
+    plan = PatPlan.from_units(table, units, spec.num_heads, spec.num_kv_heads, spec.head_dim, split=split)
+    try:
+        kc, vc = kv_pool_from_store(kv_store, table.block_size, dtype, device)
+        qt = torch.from_numpy(np.ascontiguousarray(q, dtype=np.float32)).to(device=device, dtype=dtype)
+        out = pat_attention(plan, qt, kc, vc)
+        torch.cuda.synchronize(qt.device)
+        return out.to(torch.float64).cpu().numpy()
+    finally:
+        plan.close()
+
+
+__all__ = ["run_packed_attention", "pat_attention", "PatDecoder", "kv_pool_from_store", "CoverageGap"]

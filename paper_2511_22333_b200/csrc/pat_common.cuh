@@ -1,0 +1,44 @@
+// Shared definitions for the PAT (pack -> forward -> merge) native library.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "../../include/pat.h"
+
+#define PAT_HD __host__ __device__ __forceinline__
+
+namespace pat {
+
+// Thread-local error message for pat_last_error().
+void set_error(const char* fmt, ...);
+
+// Rows view: row q is blk[row_begin(q) .. row_begin(q) + nblk[q]); the last
+// block holds valid[q] tokens.  Either CSR (off != nullptr) or fixed stride.
+struct RowsView {
+  const int32_t* blk;
+  const int64_t* off;   // CSR offsets (B+1) or nullptr
+  int64_t stride;       // used when off == nullptr
+  const int32_t* nblk;  // blocks per row
+  const int32_t* valid; // valid tokens in the last block, in [1, bs]
+  int B;
+  int bs;
+
+  PAT_HD int64_t row_begin(int q) const { return off ? off[q] : (int64_t)q * stride; }
+  PAT_HD int32_t block(int q, int p) const { return blk[row_begin(q) + p]; }
+  PAT_HD int32_t tokens_at(int q, int p) const { return p == nblk[q] - 1 ? valid[q] : bs; }
+  PAT_HD bool same_unit(int q, int r, int p) const {
+    return block(q, p) == block(r, p) && tokens_at(q, p) == tokens_at(r, p);
+  }
+  // tokens covered by positions [a, b) of row q
+  PAT_HD int64_t span_tokens(int q, int a, int b) const {
+    int64_t t = (int64_t)(b - a) * bs;
+    if (b == nblk[q] && b > a) t -= (bs - valid[q]);
+    return t;
+  }
+};
+
+PAT_HD int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace pat

@@ -1,0 +1,448 @@
+// Streaming forward kernel for packs whose query tile is narrow (rows = q*G <= 64
+// per CTA) and the online-softmax merge kernel.
+//
+// One CTA (4 warps) owns one work item = (forward unit, kv head, row block) and
+// computes, for each of its rows (query i of the pack, head kvh*G+g), the
+// partial (max, exp-sum, weighted V sum) of cta_partial (attention.py:140-163)
+// over the unit's KV span -- online, in 64-token stages:
+//   * every K/V page of the stage is copied ONCE per CTA into shared memory
+//     (16-byte cp.async, 128B-swizzled rows, 3-stage ring) and shared by all
+//     rows of the pack (this is what packing buys: one load of a shared prefix
+//     for all its queries);
+//   * S = Q K^T and O += P V run on tensor cores with mma.sync m16n8k16
+//     (Q rows padded to 16); fp32 accumulate, P rounded to the input dtype;
+//   * the warps of one 16-row tile split the stage's tokens and are combined
+//     at the end in shared memory.
+// A row whose query is covered by this unit only is normalised and written to
+// the output directly; otherwise (o/l, log2-sum-exp) goes to its fp32 slot and
+// the merge kernel folds the slots (_merge_batch_into, attention.py:187-199).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "pat_plan.cuh"
+
+namespace pat {
+
+constexpr int kThreads = 128;
+constexpr int kStageTok = 64;
+constexpr int kStages = 3;
+
+template <typename T> struct Vec2;
+template <> struct Vec2<__half> {
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+template <> struct Vec2<__nv_bfloat16> {
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1);
+
+template <>
+__device__ __forceinline__ void mma16816<__half>(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+template <>
+__device__ __forceinline__ void mma16816<__nv_bfloat16>(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t* r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Shared-memory tiles hold 16-bit rows split into 64-element (128-byte) lines:
+// a K/V stage is [page][D/64 halves][16 tokens][64], the Q tile [D/64][rows][64].
+// The 16-byte chunk c of a line is stored at c ^ (row & 7) -- the TMA/UMMA
+// 128B swizzle pattern (line index mod 8 == row mod 8 in these layouts), which
+// makes every ldmatrix phase (8 consecutive rows, same chunk) conflict-free.
+template <int D>
+__device__ __forceinline__ uint32_t swz_kv(int t, int ch) {
+  int line = (t >> 4) * (D / 64) * 16 + (ch >> 3) * 16 + (t & 15);
+  return (uint32_t)(line * 128 + (((ch & 7) ^ (t & 7)) << 4));
+}
+template <int ROWS>
+__device__ __forceinline__ uint32_t swz_q(int r, int ch) {
+  int line = (ch >> 3) * ROWS + r;
+  return (uint32_t)(line * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
+
+template <int WM, int D, typename T>
+struct FwdSmem {
+  static constexpr int kTileBytes = kStageTok * D * 2;  // one K or V stage
+  static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int kQBytes = WM * 16 * D * 2;
+  static constexpr int kBytes = kStages * kStageBytes + kQBytes;
+  // epilogue reuse of the stage ring: 4 warps x 16 rows x D fp32 + row stats
+  static_assert(4 * 16 * D * 4 + 2 * 4 * 16 * 4 <= kStages * kStageBytes, "epilogue scratch");
+};
+
+template <int WM, int D, typename T>
+__global__ void __launch_bounds__(kThreads, 2)
+    fwd_mma_kernel(DevPlan plan, int var, const T* __restrict__ qg, const T* __restrict__ kc,
+                   const T* __restrict__ vc, T* __restrict__ out, float* __restrict__ part_o,
+                   float* __restrict__ part_lse, float scale_log2) {
+  using S = FwdSmem<WM, D, T>;
+  constexpr int WN = 4 / WM;          // warps sharing one row tile
+  constexpr int TW = kStageTok / WN;  // tokens per warp per stage
+  constexpr int NT = TW / 8;          // score n-tiles per warp
+  constexpr int KS = D / 16;          // k-steps over head_dim
+  constexpr int CH = D / 8;           // 16-byte chunks per token row
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t sq = sbase + kStages * S::kStageBytes;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mt = warp / WN, wn = warp % WN;
+  const int H = plan.H, KVH = plan.KVH, G = plan.G, bs = plan.bs;
+  const int n_items = plan.n_items[var];
+  const Item* items = plan.items[var];
+
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const Item item = items[it];
+    const int u = item.unit, h = item.kvh;
+    const int p = plan.unit_pack[u];
+    const int ntok = plan.unit_ntok[u];
+    const int32_t* blist = plan.pack_blk + plan.pack_blk_off[p] + plan.unit_page0[u];
+    const int qoff = plan.pack_q_off[p];
+    const int nst = (ntok + kStageTok - 1) / kStageTok;
+
+    // ---- Q tile -> smem (rows beyond nrows are zero) ----
+    for (int c = tid; c < WM * 16 * CH; c += kThreads) {
+      int r = c / CH, ch = c % CH;
+      const T* src = qg;
+      int bytes = 0;
+      if (r < item.nrows) {
+        int row = item.row0 + r;
+        int qid = plan.pack_q[qoff + row / G];
+        src = qg + ((int64_t)qid * H + h * G + row % G) * D + ch * 8;
+        bytes = 16;
+      }
+      cp_async16(sq + swz_q<WM * 16>(r, ch), src, bytes);
+    }
+    cp_commit();
+
+    auto load_stage = [&](int s) {
+      if (s < nst) {
+        const uint32_t dk = sbase + (s % kStages) * S::kStageBytes;
+        const uint32_t dv = dk + S::kTileBytes;
+#pragma unroll
+        for (int i = 0; i < kStageTok * CH / kThreads; ++i) {
+          int c = tid + i * kThreads;
+          int t = c / CH, ch = c % CH;
+          int tok = s * kStageTok + t;
+          int bytes = tok < ntok ? 16 : 0;
+          int64_t off = 0;
+          if (bytes) {
+            int b = blist[tok / bs];
+            off = (((int64_t)b * bs + tok % bs) * KVH + h) * D + ch * 8;
+          }
+          cp_async16(dk + swz_kv<D>(t, ch), kc + off, bytes);
+          cp_async16(dv + swz_kv<D>(t, ch), vc + off, bytes);
+        }
+      }
+      cp_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) load_stage(s);
+
+    // Q fragments (A operand), loaded once the first group lands.
+    cp_wait<kStages - 1>();
+    __syncthreads();
+    uint32_t qa[KS][4];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      int r = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+      int ch = ks * 2 + (lane >> 4);
+      ldsm_x4(qa[ks], sq + swz_q<WM * 16>(r, ch));
+    }
+
+    float o[D / 8][4];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+
+    for (int s = 0; s < nst; ++s) {
+      cp_wait<kStages - 2>();
+      __syncthreads();
+      load_stage(s + kStages - 1);
+      const uint32_t tk = sbase + (s % kStages) * S::kStageBytes;
+      const uint32_t tv = tk + S::kTileBytes;
+      const int t0 = wn * TW;  // warp's first token inside the stage
+
+      float sc[NT][4];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+        for (int j = 0; j < NT; j += 2) {
+          uint32_t b[4];
+          int t = t0 + j * 8 + (lane & 7) + (lane >> 4) * 8;
+          int ch = ks * 2 + ((lane >> 3) & 1);
+          ldsm_x4(b, tk + swz_kv<D>(t, ch));
+          mma16816<T>(sc[j], qa[ks], b[0], b[1]);
+          mma16816<T>(sc[j + 1], qa[ks], b[2], b[3]);
+        }
+      }
+      // mask tokens past the unit's span, online softmax in log2 units
+      const int tbase = s * kStageTok + t0 + 2 * (lane & 3);
+      float mx[2] = {mrow[0], mrow[1]};
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          int tok = tbase + j * 8 + (e & 1);
+          float v = tok < ntok ? sc[j][e] * scale_log2 : -INFINITY;
+          sc[j][e] = v;
+          mx[e >> 1] = fmaxf(mx[e >> 1], v);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      }
+      float alpha[2], muse[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        muse[r] = mx[r] == -INFINITY ? 0.f : mx[r];
+        alpha[r] = exp2f(mrow[r] - muse[r]);
+        mrow[r] = mx[r];
+        lrow[r] *= alpha[r];
+      }
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) {
+        o[i][0] *= alpha[0];
+        o[i][1] *= alpha[0];
+        o[i][2] *= alpha[1];
+        o[i][3] *= alpha[1];
+      }
+      uint32_t pa[NT / 2][4];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        float p0 = exp2f(sc[j][0] - muse[0]), p1 = exp2f(sc[j][1] - muse[0]);
+        float p2 = exp2f(sc[j][2] - muse[1]), p3 = exp2f(sc[j][3] - muse[1]);
+        lrow[0] += p0 + p1;
+        lrow[1] += p2 + p3;
+        pa[j >> 1][(j & 1) * 2 + 0] = Vec2<T>::pack(p0, p1);
+        pa[j >> 1][(j & 1) * 2 + 1] = Vec2<T>::pack(p2, p3);
+      }
+      // O += P V  (k = tokens, n = head dim)
+#pragma unroll
+      for (int kk = 0; kk < NT / 2; ++kk) {
+#pragma unroll
+        for (int dn = 0; dn < D / 16; ++dn) {
+          uint32_t b[4];
+          int t = t0 + kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+          int ch = dn * 2 + (lane >> 4);
+          ldsm_x4_t(b, tv + swz_kv<D>(t, ch));
+          mma16816<T>(o[dn * 2], pa[kk], b[0], b[1]);
+          mma16816<T>(o[dn * 2 + 1], pa[kk], b[2], b[3]);
+        }
+      }
+    }
+    cp_wait<0>();
+    __syncthreads();
+
+    // ---- epilogue: per-warp (m, l, O) -> smem, combine the WN warps of a row tile ----
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+      lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+    }
+    float* so = reinterpret_cast<float*>(smem);              // [4 warps][16][D]
+    float* sm = so + 4 * 16 * D;                              // [4][16]
+    float* sl = sm + 4 * 16;                                  // [4][16]
+    {
+      const int ra = lane >> 2, rb = ra + 8, cb = 2 * (lane & 3);
+      float* wo = so + warp * 16 * D;
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) {
+        *reinterpret_cast<float2*>(wo + ra * D + i * 8 + cb) = make_float2(o[i][0], o[i][1]);
+        *reinterpret_cast<float2*>(wo + rb * D + i * 8 + cb) = make_float2(o[i][2], o[i][3]);
+      }
+      if ((lane & 3) == 0) {
+        sm[warp * 16 + ra] = mrow[0];
+        sm[warp * 16 + rb] = mrow[1];
+        sl[warp * 16 + ra] = lrow[0];
+        sl[warp * 16 + rb] = lrow[1];
+      }
+    }
+    __syncthreads();
+    const int* uslot = plan.unit_slot + plan.unit_slot_off[u];
+    for (int c = tid; c < WM * 16 * (D / 4); c += kThreads) {
+      int r = c / (D / 4), x = (c % (D / 4)) * 4;
+      if (r >= item.nrows) continue;
+      int tile = r / 16, rr = r % 16;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < WN; ++w) M = fmaxf(M, sm[(tile * WN + w) * 16 + rr]);
+      float L = 0.f;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < WN; ++w) {
+        int ww = tile * WN + w;
+        float f = exp2f(sm[ww * 16 + rr] - M);
+        L += sl[ww * 16 + rr] * f;
+        float4 v = *reinterpret_cast<const float4*>(so + (ww * 16 + rr) * D + x);
+        acc.x += v.x * f;
+        acc.y += v.y * f;
+        acc.z += v.z * f;
+        acc.w += v.w * f;
+      }
+      const float inv = 1.f / L;
+      int row = item.row0 + r;
+      int i = row / G;
+      int qid = plan.pack_q[qoff + i];
+      int head = h * G + row % G;
+      int slot = uslot[i];
+      if (slot < 0) {
+        T* dst = out + ((int64_t)qid * H + head) * D + x;
+        uint2 pk;
+        pk.x = Vec2<T>::pack(acc.x * inv, acc.y * inv);
+        pk.y = Vec2<T>::pack(acc.z * inv, acc.w * inv);
+        *reinterpret_cast<uint2*>(dst) = pk;
+      } else {
+        float* dst = part_o + ((int64_t)slot * H + head) * D + x;
+        *reinterpret_cast<float4*>(dst) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+        if (x == 0) part_lse[(int64_t)slot * H + head] = M + log2f(L);
+      }
+    }
+    __syncthreads();  // smem reused by the next item
+  }
+}
+
+// One warp per (query, head): fold the query's slots with online softmax.
+template <int D, typename T>
+__global__ void __launch_bounds__(256) merge_kernel(DevPlan plan, const float* __restrict__ part_o,
+                                                    const float* __restrict__ part_lse, T* __restrict__ out) {
+  const int H = plan.H;
+  const int nq = *plan.n_merge;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  constexpr int PER = D / 32;
+  for (int w = gw; w < nq * H; w += nw) {
+    const int q = plan.merge_q[w / H], head = w % H;
+    const int base = plan.q_slot_off[q], n = plan.q_nslot[q];
+    float M = -INFINITY;
+    for (int i = lane; i < n; i += 32) M = fmaxf(M, part_lse[(int64_t)(base + i) * H + head]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float acc[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+    float L = 0.f;
+    for (int i = 0; i < n; ++i) {
+      const int64_t s = (int64_t)(base + i) * H + head;
+      const float f = exp2f(part_lse[s] - M);
+      L += f;
+      const float* src = part_o + s * D + lane * PER;
+#pragma unroll
+      for (int e = 0; e < PER; e += 4) {
+        float4 v = *reinterpret_cast<const float4*>(src + e);
+        acc[e] += f * v.x;
+        acc[e + 1] += f * v.y;
+        acc[e + 2] += f * v.z;
+        acc[e + 3] += f * v.w;
+      }
+    }
+    const float inv = 1.f / L;
+    T* dst = out + ((int64_t)q * H + head) * D + lane * PER;
+#pragma unroll
+    for (int e = 0; e < PER; e += 2) {
+      uint32_t pk = Vec2<T>::pack(acc[e] * inv, acc[e + 1] * inv);
+      *reinterpret_cast<uint32_t*>(dst + e) = pk;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// launchers
+// ------------------------------------------------------------------------------------------
+
+template <int WM, int D, typename T>
+static cudaError_t launch_fwd_t(const DevPlan& plan, int var, int grid, const void* q, const void* k,
+                                const void* v, void* out, float* po, float* pl, float scale_log2,
+                                cudaStream_t st) {
+  constexpr int smem = FwdSmem<WM, D, T>::kBytes;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(fwd_mma_kernel<WM, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  fwd_mma_kernel<WM, D, T><<<grid, kThreads, smem, st>>>(plan, var, (const T*)q, (const T*)k, (const T*)v,
+                                                        (T*)out, po, pl, scale_log2);
+  return cudaGetLastError();
+}
+
+template <int D, typename T>
+static cudaError_t launch_fwd_d(const DevPlan& plan, int var, int grid, const void* q, const void* k,
+                                const void* v, void* out, float* po, float* pl, float scale_log2,
+                                cudaStream_t st) {
+  switch (var) {
+    case VAR_R16: return launch_fwd_t<1, D, T>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+    case VAR_R32: return launch_fwd_t<2, D, T>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+    default: return launch_fwd_t<4, D, T>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+  }
+}
+
+cudaError_t launch_forward_variant(const DevPlan& plan, int var, int grid, int dtype, int d, const void* q,
+                                   const void* k, const void* v, void* out, float* po, float* pl,
+                                   float scale_log2, cudaStream_t st) {
+  if (dtype == PAT_DTYPE_F16) {
+    if (d == 128) return launch_fwd_d<128, __half>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+    return launch_fwd_d<64, __half>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+  }
+  if (d == 128) return launch_fwd_d<128, __nv_bfloat16>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+  return launch_fwd_d<64, __nv_bfloat16>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+}
+
+cudaError_t launch_merge(const DevPlan& plan, int grid, int dtype, int d, const float* po, const float* pl,
+                         void* out, cudaStream_t st) {
+  if (dtype == PAT_DTYPE_F16) {
+    if (d == 128) merge_kernel<128, __half><<<grid, 256, 0, st>>>(plan, po, pl, (__half*)out);
+    else merge_kernel<64, __half><<<grid, 256, 0, st>>>(plan, po, pl, (__half*)out);
+  } else {
+    if (d == 128) merge_kernel<128, __nv_bfloat16><<<grid, 256, 0, st>>>(plan, po, pl, (__nv_bfloat16*)out);
+    else merge_kernel<64, __nv_bfloat16><<<grid, 256, 0, st>>>(plan, po, pl, (__nv_bfloat16*)out);
+  }
+  return cudaGetLastError();
+}
+
+int fwd_smem_bytes(int var, int d) {
+  int wm = var == VAR_R16 ? 1 : (var == VAR_R32 ? 2 : 4);
+  return kStages * 2 * kStageTok * d * 2 + wm * 16 * d * 2;
+}
+
+}  // namespace pat

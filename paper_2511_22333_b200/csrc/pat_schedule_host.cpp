@@ -1,0 +1,139 @@
+// Host scheduler: packs -> forward units (KV split) -> partial slots -> CTA work items.
+//
+// Reference mode reproduces split_long_kv (simulator.py:117-155) on the packs
+// taken as tasks (the plan_tasks query pre-split, simulator.py:185-202, is not
+// applied: a wide pack is tiled over rows inside the kernel instead of
+// re-reading its KV per query group).  Native mode sizes parts for 148 SMs.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "pat_plan_host.h"
+
+namespace pat {
+
+namespace {
+
+struct Part {
+  int page0, npages, ntok;
+};
+
+void split_pack(int npages, int kv, int bs, int parts, std::vector<Part>& out) {
+  // near-equal block counts, larger parts first; the last part carries the
+  // partial block (simulator.py:137-154)
+  int base = npages / parts, extra = npages % parts, pos = 0, used = 0;
+  for (int i = 0; i < parts; ++i) {
+    int take = base + (i < extra ? 1 : 0);
+    int tok = std::min(take * bs, kv - used);
+    out.push_back({pos, take, tok});
+    pos += take;
+    used += tok;
+  }
+}
+
+}  // namespace
+
+int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S) {
+  const int NP = P.n_packs();
+  const int G = sp.H / sp.KVH;
+  *S = HostSchedule();
+  S->q_slot_off.assign(sp.B, 0);
+  S->q_nslot.assign(sp.B, 0);
+  S->unit_slot_off.assign(1, 0);
+
+  // 1. parts per pack
+  std::vector<int> nparts(NP, 1);
+  if (sp.split_mode == PAT_SPLIT_REFERENCE && NP > 0) {
+    int64_t tot = 0;
+    for (int p = 0; p < NP; ++p) tot += P.kv[p];
+    const double mean = (double)tot / (double)NP;
+    for (int p = 0; p < NP; ++p) {
+      if ((double)P.kv[p] <= mean) continue;
+      int parts = (int)std::ceil((double)P.kv[p] / mean);
+      int nblocks = std::max(P.blk_off[p + 1] - P.blk_off[p], (int)ceil_div(P.kv[p], sp.bs));
+      nparts[p] = std::min(parts, nblocks);
+    }
+  } else if (sp.split_mode == PAT_SPLIT_NATIVE && NP > 0) {
+    int64_t cost = 0;
+    for (int p = 0; p < NP; ++p) {
+      int rows = (P.q_off[p + 1] - P.q_off[p]) * G;
+      int R = variant_rows(choose_variant(rows));
+      cost += (int64_t)(P.blk_off[p + 1] - P.blk_off[p]) * sp.KVH * ceil_div(rows, R);
+    }
+    const int64_t slots = (int64_t)std::max(sp.num_sms, 1) * 2;
+    const int64_t chunk = std::max<int64_t>(4, ceil_div(cost, 2 * slots));
+    for (int p = 0; p < NP; ++p) {
+      int pages = P.blk_off[p + 1] - P.blk_off[p];
+      int rows = (P.q_off[p + 1] - P.q_off[p]) * G;
+      // merge traffic of an extra part (q*H*d*4 B out + in) must stay small next to
+      // its KV bytes: part tokens >= 8 * rows  <=>  intermediates <= 1/4 of KV.
+      int64_t cap = std::max<int64_t>(1, (int64_t)P.kv[p] / (8 * (int64_t)rows));
+      nparts[p] = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(pages, chunk), cap));
+      nparts[p] = std::min(nparts[p], pages);
+    }
+  }
+
+  // 2. units
+  std::vector<Part> parts;
+  std::vector<int> unit_begin(NP + 1, 0);
+  for (int p = 0; p < NP; ++p) {
+    parts.clear();
+    int pages = P.blk_off[p + 1] - P.blk_off[p];
+    split_pack(pages, P.kv[p], sp.bs, nparts[p], parts);
+    unit_begin[p + 1] = unit_begin[p] + (int)parts.size();
+    for (int i = 0; i < (int)parts.size(); ++i) {
+      S->unit_pack.push_back(p);
+      S->unit_page0.push_back(parts[i].page0);
+      S->unit_npages.push_back(parts[i].npages);
+      S->unit_ntok.push_back(parts[i].ntok);
+      S->unit_split_idx.push_back(i);
+      S->unit_split_of.push_back((int)parts.size());
+    }
+  }
+  const int NU = (int)S->unit_pack.size();
+
+  // 3. slots: a query covered by more than one unit gets one fp32 partial slot
+  // per unit, in unit order (the reference fold order, attention.py:228-235).
+  std::vector<int32_t> qcnt(sp.B, 0);
+  for (int p = 0; p < NP; ++p)
+    for (int i = P.q_off[p]; i < P.q_off[p + 1]; ++i) qcnt[P.q[i]] += nparts[p];
+  int32_t next = 0;
+  for (int q = 0; q < sp.B; ++q) {
+    if (qcnt[q] > 1) {
+      S->q_slot_off[q] = next;
+      S->q_nslot[q] = qcnt[q];
+      next += qcnt[q];
+      S->merge_q.push_back(q);
+    } else {
+      S->q_slot_off[q] = -1;
+    }
+  }
+  S->n_slots = next;
+  std::vector<int32_t> qcur(sp.B, 0);
+  for (int u = 0; u < NU; ++u) {
+    int p = S->unit_pack[u];
+    for (int i = P.q_off[p]; i < P.q_off[p + 1]; ++i) {
+      int q = P.q[i];
+      S->unit_slot.push_back(qcnt[q] > 1 ? S->q_slot_off[q] + qcur[q]++ : -1);
+    }
+    S->unit_slot_off.push_back((int32_t)S->unit_slot.size());
+  }
+
+  // 4. work items, longest first within each kernel variant
+  std::vector<int> order(NU);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return S->unit_npages[a] > S->unit_npages[b]; });
+  for (int u : order) {
+    int p = S->unit_pack[u];
+    int rows = (P.q_off[p + 1] - P.q_off[p]) * G;
+    int v = choose_variant(rows);
+    int R = variant_rows(v);
+    for (int r0 = 0; r0 < rows; r0 += R)
+      for (int h = 0; h < sp.KVH; ++h) S->items[v].push_back({u, h, r0, std::min(R, rows - r0)});
+  }
+  (void)unit_begin;
+  return PAT_OK;
+}
+
+}  // namespace pat
