@@ -24,7 +24,8 @@ u8p = C.POINTER(C.c_uint8)
 
 class PlanOptions(C.Structure):
     _fields_ = [("num_heads", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
-                ("split_mode", C.c_int32), ("num_sms", C.c_int32), ("flags", C.c_int32)]
+                ("split_mode", C.c_int32), ("num_sms", C.c_int32), ("flags", C.c_int32),
+                ("tc_min_rows", C.c_int32)]
 
 
 class PlanInfo(C.Structure):

@@ -73,9 +73,10 @@ class PatDecoder:
     """Serving-side helper: plan cache (lazy update) + reusable workspace."""
 
     def __init__(self, num_heads: int, num_kv_heads: int, head_dim: int, split: str = "native",
-                 device: Union[str, torch.device] = "cuda"):
+                 device: Union[str, torch.device] = "cuda", tc_min_rows: int = 0):
         self.num_heads, self.num_kv_heads, self.head_dim = num_heads, num_kv_heads, head_dim
         self.split = split
+        self.tc_min_rows = tc_min_rows
         self.device = torch.device(device)
         self.cache = PackCache()
         self._ws: Optional[torch.Tensor] = None
@@ -84,7 +85,8 @@ class PatDecoder:
         fp = table.fingerprint()
         plan = self.cache.lookup(fp)
         if plan is None:
-            plan = PatPlan.from_table(table, self.num_heads, self.num_kv_heads, self.head_dim, split=self.split)
+            plan = PatPlan.from_table(table, self.num_heads, self.num_kv_heads, self.head_dim, split=self.split,
+                                      tc_min_rows=self.tc_min_rows)
             self.cache.store(fp, plan)
         return plan
 
@@ -117,7 +119,7 @@ def kv_pool_from_store(kv_store: dict, block_size: int, dtype=torch.float16, dev
 def run_packed_attention(table: BlockTable, partition_or_tasks: Union[Partition, Sequence[CtaTask], Sequence[CtaPack]],
                          kv_store: dict, q: np.ndarray, spec: WorkloadSpec, intermediate_dtype=None,
                          *, dtype: torch.dtype = torch.float16, split: str = "none",
-                         device: Union[str, torch.device] = "cuda") -> np.ndarray:
+                         device: Union[str, torch.device] = "cuda", tc_min_rows: int = 0) -> np.ndarray:
     """Drop-in for ``prefixpack.run_packed_attention`` (``attention.py:202-239``).
 
     Coverage is checked natively (``CoverageGap``); partials are always fp32 on
@@ -130,7 +132,8 @@ def run_packed_attention(table: BlockTable, partition_or_tasks: Union[Partition,
         raise ShapeMismatch("Q row count must match the table")
     if table.num_queries == 0:
         return np.zeros(q.shape, dtype=np.float64)
-    plan = PatPlan.from_units(table, units, spec.num_heads, spec.num_kv_heads, spec.head_dim, split=split)
+    plan = PatPlan.from_units(table, units, spec.num_heads, spec.num_kv_heads, spec.head_dim, split=split,
+                              tc_min_rows=tc_min_rows)
     try:
         kc, vc = kv_pool_from_store(kv_store, table.block_size, dtype, device)
         qt = torch.from_numpy(np.ascontiguousarray(q, dtype=np.float32)).to(device=device, dtype=dtype)

@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "pat_plan_host.h"
 
 namespace pat {
@@ -28,6 +30,10 @@ cudaError_t launch_forward_variant(const DevPlan& plan, int var, int grid, int d
 cudaError_t launch_merge(const DevPlan& plan, int grid, int dtype, int d, const float* po, const float* pl,
                          void* out, cudaStream_t st);
 int fwd_smem_bytes(int var, int d);
+cudaError_t launch_forward_tc(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var, int grid,
+                              int dtype, int d, const void* q, void* out, float* po, float* pl, float scale_log2,
+                              cudaStream_t st);
+int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t num_blocks, int bs, int kvh, int d, int dtype);
 
 }  // namespace pat
 
@@ -43,19 +49,25 @@ using namespace pat;
   } while (0)
 
 struct pat_plan {
-  int B = 0, bs = 16, H = 0, KVH = 0, d = 0, split_mode = 0, num_sms = 148;
+  int B = 0, bs = 16, H = 0, KVH = 0, d = 0, split_mode = 0, num_sms = 148, tc_min_rows = 64;
   bool on_device = false;
   HostPacks packs;
   HostSchedule sched;
   int64_t unique_tokens = 0;
   int32_t n_items_total = 0, n_slots = 0, n_merge = 0;
-  int32_t items_cap[NUM_VARIANTS] = {0, 0, 0};
+  int32_t items_cap[NUM_VARIANTS] = {};
   // device
   void* dmem = nullptr;
   DevPlan dev{};
   int device = -1;
-  cudaStream_t streams[NUM_VARIANTS] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[NUM_VARIANTS] = {nullptr, nullptr, nullptr};
+  cudaStream_t streams[NUM_VARIANTS] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[NUM_VARIANTS] = {};
+  // TMA descriptors of the last (k_cache, v_cache) pair seen by pat_forward
+  CUtensorMap tmk, tmv;
+  const void* tm_k = nullptr;
+  const void* tm_v = nullptr;
+  int64_t tm_blocks = -1;
+  int tm_dtype = -1;
 };
 
 namespace {
@@ -88,6 +100,8 @@ void init_plan(pat_plan* P, int B, int bs, const pat_plan_options* opt) {
   P->d = opt->head_dim;
   P->split_mode = opt->split_mode;
   P->num_sms = opt->num_sms;
+  P->tc_min_rows = opt->tc_min_rows == 0 ? 64 : (opt->tc_min_rows < 0 ? 0 : opt->tc_min_rows);
+  if (P->d != 64 && P->d != 128) P->tc_min_rows = 0;
   if (P->num_sms <= 0) {
     int dev = 0, n = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -160,7 +174,7 @@ int upload(pat_plan* P) {
 }
 
 int finish_plan(pat_plan* P, const RowsView& R, int flags) {
-  ScheduleParams sp{P->B, P->bs, P->H, P->KVH, P->d, P->split_mode, P->num_sms};
+  ScheduleParams sp{P->B, P->bs, P->H, P->KVH, P->d, P->split_mode, P->num_sms, P->tc_min_rows};
   int st = host_schedule(P->packs, sp, &P->sched);
   if (st) return st;
   P->n_slots = P->sched.n_slots;
@@ -369,14 +383,29 @@ int pat_forward(const pat_plan* Pc, const void* q, const void* k_cache, const vo
   int active[NUM_VARIANTS], na = 0;
   for (int v = 0; v < NUM_VARIANTS; ++v)
     if (P->items_cap[v] > 0) active[na++] = v;
-  auto grid_for = [&](int v) {
-    int per_sm = 2;
-    int g = P->num_sms * per_sm;
-    return std::max(1, std::min(g, P->items_cap[v]));
+  if (P->items_cap[VAR_TC] > 0 &&
+      (P->tm_k != k_cache || P->tm_v != v_cache || P->tm_blocks != num_pool_blocks || P->tm_dtype != dtype)) {
+    int e1 = make_kv_tensor_map(&P->tmk, k_cache, num_pool_blocks, P->bs, P->KVH, P->d, dtype);
+    int e2 = make_kv_tensor_map(&P->tmv, v_cache, num_pool_blocks, P->bs, P->KVH, P->d, dtype);
+    if (e1 || e2) {
+      set_error("cuTensorMapEncodeTiled failed (%d, %d)", e1, e2);
+      return PAT_ERR_CUDA;
+    }
+    P->tm_k = k_cache;
+    P->tm_v = v_cache;
+    P->tm_blocks = num_pool_blocks;
+    P->tm_dtype = dtype;
+  }
+  auto launch = [&](int v, cudaStream_t sv) -> cudaError_t {
+    if (v == VAR_TC) {
+      int grid = std::max(1, std::min(P->num_sms, P->items_cap[v]));
+      return launch_forward_tc(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sv);
+    }
+    int grid = std::max(1, std::min(P->num_sms * 2, P->items_cap[v]));
+    return launch_forward_variant(P->dev, v, grid, dtype, P->d, q, k_cache, v_cache, out, po, pl, scale_log2, sv);
   };
   if (na == 1) {
-    CUDA_TRY(launch_forward_variant(P->dev, active[0], grid_for(active[0]), dtype, P->d, q, k_cache, v_cache, out,
-                                    po, pl, scale_log2, st));
+    CUDA_TRY(launch(active[0], st));
   } else if (na > 1) {
     // multi-stream forward (section 6): one stream per kernel config,
     // forked from and joined back into the caller's stream.
@@ -392,8 +421,7 @@ int pat_forward(const pat_plan* Pc, const void* q, const void* k_cache, const vo
       int v = active[i];
       cudaStream_t sv = i == 0 ? st : P->streams[v];
       if (i) CUDA_TRY(cudaStreamWaitEvent(sv, P->ev_fork, 0));
-      CUDA_TRY(launch_forward_variant(P->dev, v, grid_for(v), dtype, P->d, q, k_cache, v_cache, out, po, pl,
-                                      scale_log2, sv));
+      CUDA_TRY(launch(v, sv));
       if (i) CUDA_TRY(cudaEventRecord(P->ev_join[v], sv));
     }
     for (int i = 1; i < na; ++i) CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join[active[i]], 0));

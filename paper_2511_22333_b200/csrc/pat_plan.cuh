@@ -11,11 +11,18 @@ namespace pat {
 
 // Kernel variants: rows of a work item = (#queries x G) rounded to a row tile.
 //   V16 / V32 / V64: mma.sync m16n8k16 streaming kernel with 1 / 2 / 4 row tiles
-//   of 16 rows per CTA (4 warps; the warps of a row tile split the KV tile).
-enum Variant : int { VAR_R16 = 0, VAR_R32 = 1, VAR_R64 = 2, NUM_VARIANTS = 3 };
+//   of 16 rows per CTA (4 warps; the warps of a row tile split the KV tile);
+//   TC: tcgen05 kernel, 128-row tiles, for packs wide enough to fill them.
+enum Variant : int { VAR_R16 = 0, VAR_R32 = 1, VAR_R64 = 2, VAR_TC = 3, NUM_VARIANTS = 4 };
 
-PAT_HD int variant_rows(int v) { return v == VAR_R16 ? 16 : (v == VAR_R32 ? 32 : 64); }
-PAT_HD int choose_variant(int rows) { return rows <= 16 ? VAR_R16 : (rows <= 32 ? VAR_R32 : VAR_R64); }
+PAT_HD int variant_rows(int v) {
+  return v == VAR_R16 ? 16 : (v == VAR_R32 ? 32 : (v == VAR_R64 ? 64 : 128));
+}
+// Packs with at least `tc_min_rows` rows go to the tensor-core kernel.
+PAT_HD int choose_variant(int rows, int tc_min_rows) {
+  if (tc_min_rows > 0 && rows >= tc_min_rows) return VAR_TC;
+  return rows <= 16 ? VAR_R16 : (rows <= 32 ? VAR_R32 : VAR_R64);
+}
 
 // Work item: unit, kv head, first row, row count (rows = query_in_pack * G + g).
 struct Item {

@@ -35,6 +35,7 @@ int64_t distinct_tokens(const RowsView& R);
 
 struct ScheduleParams {
   int B, bs, H, KVH, d, split_mode, num_sms;
+  int tc_min_rows;  // rows threshold of the tcgen05 variant (0 = off)
 };
 int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* out);
 

@@ -54,22 +54,37 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S)
       nparts[p] = std::min(parts, nblocks);
     }
   } else if (sp.split_mode == PAT_SPLIT_NATIVE && NP > 0) {
-    int64_t cost = 0;
+    // Cost of a work item ~ its pages (one 8 KB K+V page slice per kv head costs
+    // about the same on either kernel); aim for >= 2 waves of items over the SMs.
+    int64_t cost = 0, kv_bytes = 0;
+    std::vector<int> rows(NP), pages(NP);
     for (int p = 0; p < NP; ++p) {
-      int rows = (P.q_off[p + 1] - P.q_off[p]) * G;
-      int R = variant_rows(choose_variant(rows));
-      cost += (int64_t)(P.blk_off[p + 1] - P.blk_off[p]) * sp.KVH * ceil_div(rows, R);
+      rows[p] = (P.q_off[p + 1] - P.q_off[p]) * G;
+      pages[p] = P.blk_off[p + 1] - P.blk_off[p];
+      int R = variant_rows(choose_variant(rows[p], sp.tc_min_rows));
+      cost += (int64_t)pages[p] * sp.KVH * ceil_div(rows[p], R);
+      kv_bytes += (int64_t)P.kv[p] * sp.KVH * sp.d * 4;
     }
     const int64_t slots = (int64_t)std::max(sp.num_sms, 1) * 2;
     const int64_t chunk = std::max<int64_t>(4, ceil_div(cost, 2 * slots));
-    for (int p = 0; p < NP; ++p) {
-      int pages = P.blk_off[p + 1] - P.blk_off[p];
-      int rows = (P.q_off[p + 1] - P.q_off[p]) * G;
-      // merge traffic of an extra part (q*H*d*4 B out + in) must stay small next to
-      // its KV bytes: part tokens >= 8 * rows  <=>  intermediates <= 1/4 of KV.
-      int64_t cap = std::max<int64_t>(1, (int64_t)P.kv[p] / (8 * (int64_t)rows));
-      nparts[p] = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(pages, chunk), cap));
-      nparts[p] = std::min(nparts[p], pages);
+    for (int p = 0; p < NP; ++p) nparts[p] = (int)std::min<int64_t>(pages[p], ceil_div(pages[p], chunk));
+    // Global merge-traffic budget: every extra part of pack p writes and re-reads
+    // q*H*d fp32 partials.  Keep the extra bytes under 1/4 of the layer's KV
+    // bytes; drop the splits with the worst partial-bytes-per-KV-byte first.
+    auto extra = [&](int p) { return (int64_t)(nparts[p] - 1) * (P.q_off[p + 1] - P.q_off[p]) * sp.H * sp.d * 8; };
+    int64_t total_extra = 0;
+    for (int p = 0; p < NP; ++p) total_extra += extra(p);
+    if (total_extra * 4 > kv_bytes) {
+      std::vector<int> ord(NP);
+      std::iota(ord.begin(), ord.end(), 0);
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+        return (int64_t)rows[a] * pages[b] > (int64_t)rows[b] * pages[a];
+      });
+      for (int p : ord) {
+        if (total_extra * 4 <= kv_bytes) break;
+        total_extra -= extra(p);
+        nparts[p] = 1;
+      }
     }
   }
 
@@ -127,7 +142,7 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S)
   for (int u : order) {
     int p = S->unit_pack[u];
     int rows = (P.q_off[p + 1] - P.q_off[p]) * G;
-    int v = choose_variant(rows);
+    int v = choose_variant(rows, sp.tc_min_rows);
     int R = variant_rows(v);
     for (int r0 = 0; r0 < rows; r0 += R)
       for (int h = 0; h < sp.KVH; ++h) S->items[v].push_back({u, h, r0, std::min(R, rows - r0)});

@@ -36,18 +36,18 @@ class PatPlan:
 
     # -- construction ---------------------------------------------------------------
     @staticmethod
-    def _opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms=0):
+    def _opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms=0, tc_min_rows=0):
         if split not in N.SPLIT_MODES:
             raise InvalidSpec(f"split must be one of {sorted(N.SPLIT_MODES)}")
         return N.PlanOptions(num_heads, num_kv_heads, head_dim, N.SPLIT_MODES[split], num_sms,
-                             N.PAT_PLAN_HOST_ONLY if host_only else 0)
+                             N.PAT_PLAN_HOST_ONLY if host_only else 0, tc_min_rows)
 
     @classmethod
     def from_table(cls, table, num_heads=32, num_kv_heads=8, head_dim=128, split="native", host_only=False,
-                   num_sms=0) -> "PatPlan":
+                   num_sms=0, tc_min_rows=0) -> "PatPlan":
         """Host C++ packer (``pat_plan_create_host``) on a BlockTable."""
         off, blk, valid = table.csr()
-        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms)
+        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms, tc_min_rows)
         h = C.c_void_p()
         st = N.lib().pat_plan_create_host(len(table.rows), N.ptr(off, C.c_int64), N.ptr(blk, C.c_int32),
                                           N.ptr(valid, C.c_int32), table.block_size, C.byref(opt), C.byref(h))
@@ -56,7 +56,7 @@ class PatPlan:
 
     @classmethod
     def from_units(cls, table, units, num_heads=32, num_kv_heads=8, head_dim=128, split="none", host_only=False,
-                   num_sms=0) -> "PatPlan":
+                   num_sms=0, tc_min_rows=0) -> "PatPlan":
         """Explicit partition: ``units`` = [(query_ids, block_ids, kv_len)] in fold order."""
         off, blk, valid = table.csr()
         uq = [np.asarray(u[0], dtype=np.int32) for u in units]
@@ -68,7 +68,7 @@ class PatPlan:
         uq_all = np.concatenate(uq) if uq else np.zeros(0, np.int32)
         ub_all = np.concatenate(ub) if ub else np.zeros(0, np.int32)
         ukv = np.asarray([int(u[2]) for u in units], dtype=np.int32)
-        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms)
+        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms, tc_min_rows)
         h = C.c_void_p()
         st = N.lib().pat_plan_create_units(len(table.rows), N.ptr(off, C.c_int64), N.ptr(blk, C.c_int32),
                                            N.ptr(valid, C.c_int32), table.block_size, len(units),
