@@ -24,12 +24,11 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
-cudaError_t launch_forward_variant(const DevPlan& plan, int var, int grid, int dtype, int d, const void* q,
-                                   const void* k, const void* v, void* out, float* po, float* pl,
+cudaError_t launch_forward_variant(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var,
+                                   int grid, int dtype, int d, const void* q, void* out, float* po, float* pl,
                                    float scale_log2, cudaStream_t st);
 cudaError_t launch_merge(const DevPlan& plan, int grid, int dtype, int d, const float* po, const float* pl,
                          void* out, cudaStream_t st);
-int fwd_smem_bytes(int var, int d);
 cudaError_t launch_forward_tc(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var, int grid,
                               int dtype, int d, const void* q, void* out, float* po, float* pl, float scale_log2,
                               cudaStream_t st);
@@ -383,8 +382,7 @@ int pat_forward(const pat_plan* Pc, const void* q, const void* k_cache, const vo
   int active[NUM_VARIANTS], na = 0;
   for (int v = 0; v < NUM_VARIANTS; ++v)
     if (P->items_cap[v] > 0) active[na++] = v;
-  if (P->items_cap[VAR_TC] > 0 &&
-      (P->tm_k != k_cache || P->tm_v != v_cache || P->tm_blocks != num_pool_blocks || P->tm_dtype != dtype)) {
+  if ((P->tm_k != k_cache || P->tm_v != v_cache || P->tm_blocks != num_pool_blocks || P->tm_dtype != dtype)) {
     int e1 = make_kv_tensor_map(&P->tmk, k_cache, num_pool_blocks, P->bs, P->KVH, P->d, dtype);
     int e2 = make_kv_tensor_map(&P->tmv, v_cache, num_pool_blocks, P->bs, P->KVH, P->d, dtype);
     if (e1 || e2) {
@@ -401,8 +399,8 @@ int pat_forward(const pat_plan* Pc, const void* q, const void* k_cache, const vo
       int grid = std::max(1, std::min(P->num_sms, P->items_cap[v]));
       return launch_forward_tc(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sv);
     }
-    int grid = std::max(1, std::min(P->num_sms * 2, P->items_cap[v]));
-    return launch_forward_variant(P->dev, v, grid, dtype, P->d, q, k_cache, v_cache, out, po, pl, scale_log2, sv);
+    int grid = std::max(1, std::min(P->num_sms, P->items_cap[v]));
+    return launch_forward_variant(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sv);
   };
   if (na == 1) {
     CUDA_TRY(launch(active[0], st));

@@ -16,6 +16,7 @@
 // A row whose query is covered by this unit only is normalised and written to
 // the output directly; otherwise (o/l, log2-sum-exp) goes to its fp32 slot and
 // the merge kernel folds the slots (_merge_batch_into, attention.py:187-199).
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -23,9 +24,7 @@
 
 namespace pat {
 
-constexpr int kThreads = 128;
 constexpr int kStageTok = 64;
-constexpr int kStages = 3;
 
 template <typename T> struct Vec2;
 template <> struct Vec2<__half> {
@@ -94,89 +93,153 @@ __device__ __forceinline__ uint32_t swz_q(int r, int ch) {
   return (uint32_t)(line * 128 + (((ch & 7) ^ (r & 7)) << 4));
 }
 
-template <int WM, int D, typename T>
-struct FwdSmem {
-  static constexpr int kTileBytes = kStageTok * D * 2;  // one K or V stage
+template <int WM, int D>
+struct StreamSmem {
+  static constexpr int KB = D / 64;
+  static constexpr int kTileBytes = kStageTok * D * 2;  // one K or V stage tile
   static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int kNumStages = D == 128 ? 5 : 8;
   static constexpr int kQBytes = WM * 16 * D * 2;
-  static constexpr int kBytes = kStages * kStageBytes + kQBytes;
-  // epilogue reuse of the stage ring: 4 warps x 16 rows x D fp32 + row stats
-  static_assert(4 * 16 * D * 4 + 2 * 4 * 16 * 4 <= kStages * kStageBytes, "epilogue scratch");
+  static constexpr int kScratchBytes = 4 * 16 * D * 4 + 2 * 4 * 16 * 4;  // epilogue: per-warp O, m, l
+  static constexpr int kOffQ = kNumStages * kStageBytes;
+  static constexpr int kOffScratch = kOffQ + kQBytes;
+  static constexpr int kOffBar = kOffScratch + kScratchBytes;
+  static constexpr int kBytes = kOffBar + 2 * kNumStages * 8 + 64;
+  static constexpr int kAlloc = kBytes + 1024;
 };
 
+constexpr int kStreamThreads = 160;  // warps 0-3 consumers (mma.sync), warp 4 TMA producer
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* tmap, uint32_t bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n)); }
+
+// Streaming forward: one TMA producer warp runs ahead through the CTA's items
+// (prefetching the next item's pages while the current one finishes), four
+// mma.sync consumer warps compute.  Stage = 64 tokens of K and V for one kv head
+// in the [16-token group][D/64][16][64] swizzled layout (one TMA box per group
+// and 64-column half).
 template <int WM, int D, typename T>
-__global__ void __launch_bounds__(kThreads, 2)
-    fwd_mma_kernel(DevPlan plan, int var, const T* __restrict__ qg, const T* __restrict__ kc,
-                   const T* __restrict__ vc, T* __restrict__ out, float* __restrict__ part_o,
-                   float* __restrict__ part_lse, float scale_log2) {
-  using S = FwdSmem<WM, D, T>;
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    fwd_stream_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                      DevPlan plan, int var, const T* __restrict__ qg, T* __restrict__ out,
+                      float* __restrict__ part_o, float* __restrict__ part_lse, float scale_log2) {
+  using S = StreamSmem<WM, D>;
+  constexpr int NS = S::kNumStages;
   constexpr int WN = 4 / WM;          // warps sharing one row tile
   constexpr int TW = kStageTok / WN;  // tokens per warp per stage
   constexpr int NT = TW / 8;          // score n-tiles per warp
   constexpr int KS = D / 16;          // k-steps over head_dim
   constexpr int CH = D / 8;           // 16-byte chunks per token row
 
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t sq = sbase + kStages * S::kStageBytes;
+  const uint32_t sq = sbase + S::kOffQ;
+  const uint32_t full0 = sbase + S::kOffBar, empty0 = full0 + NS * 8;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int mt = warp / WN, wn = warp % WN;
-  const int H = plan.H, KVH = plan.KVH, G = plan.G, bs = plan.bs;
+  const int H = plan.H, G = plan.G, bs = plan.bs;
   const int n_items = plan.n_items[var];
   const Item* items = plan.items[var];
 
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmk) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmv) : "memory");
+      uint32_t g = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item item = items[it];
+        const int u = item.unit, h = item.kvh, p = plan.unit_pack[u];
+        const int ntok = plan.unit_ntok[u];
+        const int32_t* blist = plan.pack_blk + plan.pack_blk_off[p] + plan.unit_page0[u];
+        const int nst = (ntok + kStageTok - 1) / kStageTok;
+        for (int st = 0; st < nst; ++st, ++g) {
+          const int s = g % NS;
+          mbar_wait(empty0 + 8 * s, ((g / NS) & 1) ^ 1);
+          const int rem = ntok - st * kStageTok;
+          const int ngrp = rem >= kStageTok ? kStageTok / 16 : (rem + 15) / 16;
+          const uint32_t dk = sbase + s * S::kStageBytes, dv = dk + S::kTileBytes;
+          mbar_expect_tx(full0 + 8 * s, (uint32_t)(ngrp * S::KB * 2048 * 2));
+          for (int gr = 0; gr < ngrp; ++gr) {
+            const int tok = st * kStageTok + gr * 16;
+            const int blk = __ldg(blist + tok / bs);
+            const int off = tok % bs;
+#pragma unroll
+            for (int kb = 0; kb < S::KB; ++kb) {
+              const uint32_t o = (uint32_t)((gr * S::KB + kb) * 2048);
+              tma_load_4d(dk + o, &tmk, full0 + 8 * s, kb * 64, h, off, blk);
+              tma_load_4d(dv + o, &tmv, full0 + 8 * s, kb * 64, h, off, blk);
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int mt = warp / WN, wn = warp % WN;
+  uint32_t g = 0;
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
     const Item item = items[it];
     const int u = item.unit, h = item.kvh;
     const int p = plan.unit_pack[u];
     const int ntok = plan.unit_ntok[u];
-    const int32_t* blist = plan.pack_blk + plan.pack_blk_off[p] + plan.unit_page0[u];
     const int qoff = plan.pack_q_off[p];
     const int nst = (ntok + kStageTok - 1) / kStageTok;
 
     // ---- Q tile -> smem (rows beyond nrows are zero) ----
-    for (int c = tid; c < WM * 16 * CH; c += kThreads) {
+    named_sync(1, 128);  // previous item's ldmatrix of Q and scratch reads are done
+    for (int c = tid; c < WM * 16 * CH; c += 128) {
       int r = c / CH, ch = c % CH;
-      const T* src = qg;
-      int bytes = 0;
+      uint4 v = make_uint4(0, 0, 0, 0);
       if (r < item.nrows) {
         int row = item.row0 + r;
-        int qid = plan.pack_q[qoff + row / G];
-        src = qg + ((int64_t)qid * H + h * G + row % G) * D + ch * 8;
-        bytes = 16;
+        int qid = __ldg(plan.pack_q + qoff + row / G);
+        v = __ldg(reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + h * G + row % G) * D) + ch);
       }
-      cp_async16(sq + swz_q<WM * 16>(r, ch), src, bytes);
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(sq + swz_q<WM * 16>(r, ch)), "r"(v.x),
+                   "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
     }
-    cp_commit();
-
-    auto load_stage = [&](int s) {
-      if (s < nst) {
-        const uint32_t dk = sbase + (s % kStages) * S::kStageBytes;
-        const uint32_t dv = dk + S::kTileBytes;
-#pragma unroll
-        for (int i = 0; i < kStageTok * CH / kThreads; ++i) {
-          int c = tid + i * kThreads;
-          int t = c / CH, ch = c % CH;
-          int tok = s * kStageTok + t;
-          int bytes = tok < ntok ? 16 : 0;
-          int64_t off = 0;
-          if (bytes) {
-            int b = blist[tok / bs];
-            off = (((int64_t)b * bs + tok % bs) * KVH + h) * D + ch * 8;
-          }
-          cp_async16(dk + swz_kv<D>(t, ch), kc + off, bytes);
-          cp_async16(dv + swz_kv<D>(t, ch), vc + off, bytes);
-        }
-      }
-      cp_commit();
-    };
-#pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) load_stage(s);
-
-    // Q fragments (A operand), loaded once the first group lands.
-    cp_wait<kStages - 1>();
-    __syncthreads();
+    named_sync(1, 128);
     uint32_t qa[KS][4];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
@@ -190,13 +253,24 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
     float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
 
-    for (int s = 0; s < nst; ++s) {
-      cp_wait<kStages - 2>();
-      __syncthreads();
-      load_stage(s + kStages - 1);
-      const uint32_t tk = sbase + (s % kStages) * S::kStageBytes;
+    for (int st = 0; st < nst; ++st, ++g) {
+      const int s = g % NS;
+      mbar_wait(full0 + 8 * s, (g / NS) & 1);
+      const uint32_t tk = sbase + s * S::kStageBytes;
       const uint32_t tv = tk + S::kTileBytes;
       const int t0 = wn * TW;  // warp's first token inside the stage
+      const int valid = ntok - st * kStageTok;
+      if (valid < t0 + TW) {
+        // tail: rows past the span hold stale/garbage bytes; zero this warp's V rows
+        // so that P == 0 cannot meet a NaN
+        for (int c = lane; c < TW * CH; c += 32) {
+          int t = t0 + c / CH, ch = c % CH;
+          if (t >= valid)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};\n" ::"r"(tv + swz_kv<D>(t, ch)), "r"(0)
+                         : "memory");
+        }
+        __syncwarp();
+      }
 
       float sc[NT][4];
 #pragma unroll
@@ -213,15 +287,14 @@ __global__ void __launch_bounds__(kThreads, 2)
           mma16816<T>(sc[j + 1], qa[ks], b[2], b[3]);
         }
       }
-      // mask tokens past the unit's span, online softmax in log2 units
-      const int tbase = s * kStageTok + t0 + 2 * (lane & 3);
+      const int tbase = t0 + 2 * (lane & 3);
       float mx[2] = {mrow[0], mrow[1]};
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           int tok = tbase + j * 8 + (e & 1);
-          float v = tok < ntok ? sc[j][e] * scale_log2 : -INFINITY;
+          float v = tok < valid ? sc[j][e] * scale_log2 : -INFINITY;
           sc[j][e] = v;
           mx[e >> 1] = fmaxf(mx[e >> 1], v);
         }
@@ -256,7 +329,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         pa[j >> 1][(j & 1) * 2 + 0] = Vec2<T>::pack(p0, p1);
         pa[j >> 1][(j & 1) * 2 + 1] = Vec2<T>::pack(p2, p3);
       }
-      // O += P V  (k = tokens, n = head dim)
 #pragma unroll
       for (int kk = 0; kk < NT / 2; ++kk) {
 #pragma unroll
@@ -269,19 +341,19 @@ __global__ void __launch_bounds__(kThreads, 2)
           mma16816<T>(o[dn * 2 + 1], pa[kk], b[2], b[3]);
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * s);
     }
-    cp_wait<0>();
-    __syncthreads();
 
-    // ---- epilogue: per-warp (m, l, O) -> smem, combine the WN warps of a row tile ----
+    // ---- epilogue: combine the WN warps of each row tile through scratch ----
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
       lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
     }
-    float* so = reinterpret_cast<float*>(smem);              // [4 warps][16][D]
-    float* sm = so + 4 * 16 * D;                              // [4][16]
-    float* sl = sm + 4 * 16;                                  // [4][16]
+    float* so = reinterpret_cast<float*>(smem + S::kOffScratch);  // [4 warps][16][D]
+    float* sm = so + 4 * 16 * D;                                  // [4][16]
+    float* sl = sm + 4 * 16;                                      // [4][16]
     {
       const int ra = lane >> 2, rb = ra + 8, cb = 2 * (lane & 3);
       float* wo = so + warp * 16 * D;
@@ -297,9 +369,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         sl[warp * 16 + rb] = lrow[1];
       }
     }
-    __syncthreads();
+    named_sync(1, 128);
     const int* uslot = plan.unit_slot + plan.unit_slot_off[u];
-    for (int c = tid; c < WM * 16 * (D / 4); c += kThreads) {
+    for (int c = tid; c < WM * 16 * (D / 4); c += 128) {
       int r = c / (D / 4), x = (c % (D / 4)) * 4;
       if (r >= item.nrows) continue;
       int tile = r / 16, rr = r % 16;
@@ -337,7 +409,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (x == 0) part_lse[(int64_t)slot * H + head] = M + log2f(L);
       }
     }
-    __syncthreads();  // smem reused by the next item
   }
 }
 
@@ -391,41 +462,42 @@ __global__ void __launch_bounds__(256) merge_kernel(DevPlan plan, const float* _
 // ------------------------------------------------------------------------------------------
 
 template <int WM, int D, typename T>
-static cudaError_t launch_fwd_t(const DevPlan& plan, int var, int grid, const void* q, const void* k,
-                                const void* v, void* out, float* po, float* pl, float scale_log2,
+static cudaError_t launch_fwd_t(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var,
+                                int grid, const void* q, void* out, float* po, float* pl, float scale_log2,
                                 cudaStream_t st) {
-  constexpr int smem = FwdSmem<WM, D, T>::kBytes;
+  constexpr int smem = StreamSmem<WM, D>::kAlloc;
   static bool init = false;
   if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(fwd_mma_kernel<WM, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(fwd_stream_kernel<WM, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     init = true;
   }
-  fwd_mma_kernel<WM, D, T><<<grid, kThreads, smem, st>>>(plan, var, (const T*)q, (const T*)k, (const T*)v,
-                                                        (T*)out, po, pl, scale_log2);
+  fwd_stream_kernel<WM, D, T><<<grid, kStreamThreads, smem, st>>>(tmk, tmv, plan, var, (const T*)q, (T*)out, po,
+                                                                  pl, scale_log2);
   return cudaGetLastError();
 }
 
 template <int D, typename T>
-static cudaError_t launch_fwd_d(const DevPlan& plan, int var, int grid, const void* q, const void* k,
-                                const void* v, void* out, float* po, float* pl, float scale_log2,
+static cudaError_t launch_fwd_d(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var,
+                                int grid, const void* q, void* out, float* po, float* pl, float scale_log2,
                                 cudaStream_t st) {
   switch (var) {
-    case VAR_R16: return launch_fwd_t<1, D, T>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
-    case VAR_R32: return launch_fwd_t<2, D, T>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
-    default: return launch_fwd_t<4, D, T>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+    case VAR_R16: return launch_fwd_t<1, D, T>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
+    case VAR_R32: return launch_fwd_t<2, D, T>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
+    default: return launch_fwd_t<4, D, T>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
   }
 }
 
-cudaError_t launch_forward_variant(const DevPlan& plan, int var, int grid, int dtype, int d, const void* q,
-                                   const void* k, const void* v, void* out, float* po, float* pl,
+cudaError_t launch_forward_variant(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var,
+                                   int grid, int dtype, int d, const void* q, void* out, float* po, float* pl,
                                    float scale_log2, cudaStream_t st) {
   if (dtype == PAT_DTYPE_F16) {
-    if (d == 128) return launch_fwd_d<128, __half>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
-    return launch_fwd_d<64, __half>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+    if (d == 128) return launch_fwd_d<128, __half>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
+    return launch_fwd_d<64, __half>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
   }
-  if (d == 128) return launch_fwd_d<128, __nv_bfloat16>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
-  return launch_fwd_d<64, __nv_bfloat16>(plan, var, grid, q, k, v, out, po, pl, scale_log2, st);
+  if (d == 128) return launch_fwd_d<128, __nv_bfloat16>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
+  return launch_fwd_d<64, __nv_bfloat16>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
 }
 
 cudaError_t launch_merge(const DevPlan& plan, int grid, int dtype, int d, const float* po, const float* pl,
@@ -440,9 +512,5 @@ cudaError_t launch_merge(const DevPlan& plan, int grid, int dtype, int d, const 
   return cudaGetLastError();
 }
 
-int fwd_smem_bytes(int var, int d) {
-  int wm = var == VAR_R16 ? 1 : (var == VAR_R32 ? 2 : 4);
-  return kStages * 2 * kStageTok * d * 2 + wm * 16 * d * 2;
-}
 
 }  // namespace pat

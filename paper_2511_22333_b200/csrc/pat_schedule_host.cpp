@@ -31,6 +31,62 @@ void split_pack(int npages, int kv, int bs, int parts, std::vector<Part>& out) {
   }
 }
 
+
+// Native KV split for B200.  Picks one chunk size (pages) for all packs by
+// minimising a makespan estimate over candidate chunks:
+//   max( bytes(chunk) / HBM_BW,                 -- KV + extra fp32 partials
+//        work(chunk) / num_SMs,                 -- all items spread over SMs
+//        max item cost )                        -- the critical CTA
+// + per-item fixed cost.  An item's cost is pages x per-page time of its
+// kernel (streaming: its HBM share per SM; tcgen05: per 128-row block).
+void native_parts(const HostPacks& P, const ScheduleParams& sp, std::vector<int>& nparts) {
+  const int NP = P.n_packs();
+  const int G = sp.H / sp.KVH;
+  const double bw = 6.0e3;                // bytes per ns (HBM, sustained)
+  const double page_bytes = 16.0 * sp.d * 4;  // K+V of 16 tokens of one kv head
+  const double t_stream = page_bytes / (bw / std::max(sp.num_sms, 1));  // ns per page per SM
+  const double t_tc = 350.0;              // ns per page per 128-row tcgen05 item (measured c4)
+  const double t_item = 1500.0;           // ns fixed cost per item (Q load, pipeline fill, epilogue)
+  std::vector<int> rows(NP), pages(NP), rb(NP), tc(NP);
+  int maxpages = 1;
+  double kv_bytes = 0;
+  for (int p = 0; p < NP; ++p) {
+    rows[p] = (P.q_off[p + 1] - P.q_off[p]) * G;
+    pages[p] = P.blk_off[p + 1] - P.blk_off[p];
+    int v = choose_variant(rows[p], sp.tc_min_rows);
+    tc[p] = v == VAR_TC;
+    rb[p] = (int)ceil_div(rows[p], variant_rows(v));
+    maxpages = std::max(maxpages, pages[p]);
+    kv_bytes += (double)P.kv[p] * sp.KVH * sp.d * 4;
+  }
+  std::vector<std::pair<int, double>> cand;
+  for (int chunk = 1; ; chunk *= 2) {
+    const int c = std::min(chunk, maxpages);
+    double work = 0, worst = 0, extra = 0;
+    int64_t items = 0;
+    for (int p = 0; p < NP; ++p) {
+      int parts = (int)ceil_div(pages[p], c);
+      double per_page = tc[p] ? t_tc : t_stream;
+      double item = std::min(c, pages[p]) * per_page + t_item;
+      int64_t n = (int64_t)parts * rb[p] * sp.KVH;
+      items += n;
+      work += item * n;
+      worst = std::max(worst, item);
+      if (parts > 1) extra += (double)parts * (P.q_off[p + 1] - P.q_off[p]) * sp.H * sp.d * 8;
+    }
+    double est = std::max({(kv_bytes + extra) / bw, work / std::max(sp.num_sms, 1), worst});
+    cand.emplace_back(c, est);
+    if (c >= maxpages) break;
+  }
+  double best = 1e300;
+  for (auto& ce : cand) best = std::min(best, ce.second);
+  int best_chunk = maxpages;  // the largest chunk within 2% of the best estimate: fewest splits
+  for (auto& ce : cand)
+    if (ce.second <= best * 1.02) best_chunk = std::max(best_chunk == maxpages ? 0 : best_chunk, ce.first);
+  if (best_chunk <= 0) best_chunk = maxpages;
+  for (int p = 0; p < NP; ++p) nparts[p] = (int)ceil_div(pages[p], best_chunk);
+}
+
 }  // namespace
 
 int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S) {
@@ -54,38 +110,7 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S)
       nparts[p] = std::min(parts, nblocks);
     }
   } else if (sp.split_mode == PAT_SPLIT_NATIVE && NP > 0) {
-    // Cost of a work item ~ its pages (one 8 KB K+V page slice per kv head costs
-    // about the same on either kernel); aim for >= 2 waves of items over the SMs.
-    int64_t cost = 0, kv_bytes = 0;
-    std::vector<int> rows(NP), pages(NP);
-    for (int p = 0; p < NP; ++p) {
-      rows[p] = (P.q_off[p + 1] - P.q_off[p]) * G;
-      pages[p] = P.blk_off[p + 1] - P.blk_off[p];
-      int R = variant_rows(choose_variant(rows[p], sp.tc_min_rows));
-      cost += (int64_t)pages[p] * sp.KVH * ceil_div(rows[p], R);
-      kv_bytes += (int64_t)P.kv[p] * sp.KVH * sp.d * 4;
-    }
-    const int64_t slots = (int64_t)std::max(sp.num_sms, 1) * 2;
-    const int64_t chunk = std::max<int64_t>(4, ceil_div(cost, 2 * slots));
-    for (int p = 0; p < NP; ++p) nparts[p] = (int)std::min<int64_t>(pages[p], ceil_div(pages[p], chunk));
-    // Global merge-traffic budget: every extra part of pack p writes and re-reads
-    // q*H*d fp32 partials.  Keep the extra bytes under 1/4 of the layer's KV
-    // bytes; drop the splits with the worst partial-bytes-per-KV-byte first.
-    auto extra = [&](int p) { return (int64_t)(nparts[p] - 1) * (P.q_off[p + 1] - P.q_off[p]) * sp.H * sp.d * 8; };
-    int64_t total_extra = 0;
-    for (int p = 0; p < NP; ++p) total_extra += extra(p);
-    if (total_extra * 4 > kv_bytes) {
-      std::vector<int> ord(NP);
-      std::iota(ord.begin(), ord.end(), 0);
-      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
-        return (int64_t)rows[a] * pages[b] > (int64_t)rows[b] * pages[a];
-      });
-      for (int p : ord) {
-        if (total_extra * 4 <= kv_bytes) break;
-        total_extra -= extra(p);
-        nparts[p] = 1;
-      }
-    }
+    native_parts(P, sp, nparts);
   }
 
   // 2. units
