@@ -28,15 +28,26 @@ constexpr int kStageTok = 64;
 
 template <typename T> struct Vec2;
 template <> struct Vec2<__half> {
+  // fp16 P keeps 11 significant bits: one PV pass is exact enough
+  static constexpr bool kSplitP = false;
   static __device__ __forceinline__ uint32_t pack(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
   }
+  static __device__ __forceinline__ uint32_t pack_lo(float, float, uint32_t) { return 0u; }
 };
 template <> struct Vec2<__nv_bfloat16> {
+  // bf16 P keeps 8 significant bits (2^-9 relative error, visible on peaked
+  // softmax rows): P = hi + lo, both bf16, two PV passes -> ~16-bit P
+  static constexpr bool kSplitP = true;
   static __device__ __forceinline__ uint32_t pack(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ uint32_t pack_lo(float a, float b, uint32_t hi) {
+    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&hi);
+    float2 f = __bfloat1622float2(h);
+    return pack(a - f.x, b - f.y);
   }
 };
 
@@ -180,26 +191,40 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 
   if (warp == 4) {
     // ------------------------------------------------------------ TMA producer
+    // The whole warp walks the items; lanes prefetch 32 block ids at a time
+    // (one coalesced load instead of a dependent load per page), lane 0 waits on
+    // the ring and issues the TMA boxes.
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmk) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmv) : "memory");
-      uint32_t g = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const Item item = items[it];
-        const int u = item.unit, h = item.kvh, p = plan.unit_pack[u];
-        const int ntok = plan.unit_ntok[u];
-        const int32_t* blist = plan.pack_blk + plan.pack_blk_off[p] + plan.unit_page0[u];
-        const int nst = (ntok + kStageTok - 1) / kStageTok;
-        for (int st = 0; st < nst; ++st, ++g) {
-          const int s = g % NS;
+    }
+    uint32_t g = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item item = items[it];
+      const int u = item.unit, h = item.kvh, p = plan.unit_pack[u];
+      const int ntok = plan.unit_ntok[u];
+      const int32_t* blist = plan.pack_blk + plan.pack_blk_off[p] + plan.unit_page0[u];
+      const int npages = (ntok + bs - 1) / bs;
+      const int nst = (ntok + kStageTok - 1) / kStageTok;
+      int base = -1024, blk_reg = 0;
+      for (int st = 0; st < nst; ++st, ++g) {
+        const int s = g % NS;
+        const int rem = ntok - st * kStageTok;
+        const int ngrp = rem >= kStageTok ? kStageTok / 16 : (rem + 15) / 16;
+        const uint32_t dk = sbase + s * S::kStageBytes, dv = dk + S::kTileBytes;
+        if (lane == 0) {
           mbar_wait(empty0 + 8 * s, ((g / NS) & 1) ^ 1);
-          const int rem = ntok - st * kStageTok;
-          const int ngrp = rem >= kStageTok ? kStageTok / 16 : (rem + 15) / 16;
-          const uint32_t dk = sbase + s * S::kStageBytes, dv = dk + S::kTileBytes;
           mbar_expect_tx(full0 + 8 * s, (uint32_t)(ngrp * S::KB * 2048 * 2));
-          for (int gr = 0; gr < ngrp; ++gr) {
-            const int tok = st * kStageTok + gr * 16;
-            const int blk = __ldg(blist + tok / bs);
+        }
+        for (int gr = 0; gr < ngrp; ++gr) {
+          const int tok = st * kStageTok + gr * 16;
+          const int pg = tok / bs;
+          if (pg >= base + 32) {  // warp-uniform refill of the block-id window
+            base = pg;
+            blk_reg = base + lane < npages ? __ldg(blist + base + lane) : 0;
+          }
+          const int blk = __shfl_sync(0xffffffffu, blk_reg, pg - base);
+          if (lane == 0) {
             const int off = tok % bs;
 #pragma unroll
             for (int kb = 0; kb < S::KB; ++kb) {
@@ -319,15 +344,21 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         o[i][2] *= alpha[1];
         o[i][3] *= alpha[1];
       }
-      uint32_t pa[NT / 2][4];
+      constexpr bool kSplit = Vec2<T>::kSplitP;
+      uint32_t pa[NT / 2][4], pl[kSplit ? NT / 2 : 1][4];
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         float p0 = exp2f(sc[j][0] - muse[0]), p1 = exp2f(sc[j][1] - muse[0]);
         float p2 = exp2f(sc[j][2] - muse[1]), p3 = exp2f(sc[j][3] - muse[1]);
         lrow[0] += p0 + p1;
         lrow[1] += p2 + p3;
-        pa[j >> 1][(j & 1) * 2 + 0] = Vec2<T>::pack(p0, p1);
-        pa[j >> 1][(j & 1) * 2 + 1] = Vec2<T>::pack(p2, p3);
+        const uint32_t h01 = Vec2<T>::pack(p0, p1), h23 = Vec2<T>::pack(p2, p3);
+        pa[j >> 1][(j & 1) * 2 + 0] = h01;
+        pa[j >> 1][(j & 1) * 2 + 1] = h23;
+        if constexpr (kSplit) {
+          pl[j >> 1][(j & 1) * 2 + 0] = Vec2<T>::pack_lo(p0, p1, h01);
+          pl[j >> 1][(j & 1) * 2 + 1] = Vec2<T>::pack_lo(p2, p3, h23);
+        }
       }
 #pragma unroll
       for (int kk = 0; kk < NT / 2; ++kk) {
@@ -339,6 +370,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           ldsm_x4_t(b, tv + swz_kv<D>(t, ch));
           mma16816<T>(o[dn * 2], pa[kk], b[0], b[1]);
           mma16816<T>(o[dn * 2 + 1], pa[kk], b[2], b[3]);
+          if constexpr (kSplit) {
+            mma16816<T>(o[dn * 2], pl[kk], b[0], b[1]);
+            mma16816<T>(o[dn * 2 + 1], pl[kk], b[2], b[3]);
+          }
         }
       }
       __syncwarp();

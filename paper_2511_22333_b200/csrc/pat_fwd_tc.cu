@@ -31,29 +31,34 @@ namespace tc {
 constexpr int kThreads = 256;
 constexpr int kM = 128;      // rows per tile (TMEM lanes)
 constexpr int kN = 64;       // tokens per KV tile
-constexpr int kStages = 4;   // KV ring depth
 constexpr uint32_t kTmemCols = 256;  // S0 [0,64) S1 [64,128) O [128, 128+D)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-template <int D>
+template <typename T> struct Fmt;
+
+// kSplit: bf16 P is stored as hi + lo bf16 planes (two PV MMAs per k-step).
+template <int D, bool kSplit>
 struct Layout {
   static constexpr int KB = D / 64;                 // 64-element (128 B) column blocks
+  static constexpr int kStages = kSplit ? 3 : 4;    // KV ring depth
   static constexpr int kQBytes = KB * kM * 128;     // [KB][128 rows][64]
   static constexpr int kPBytes = kM * 128;          // [128 rows][64 tokens]
+  static constexpr int kPPlanes = kSplit ? 2 : 1;
   static constexpr int kTileBytes = KB * kN * 128;  // one K or V tile: [KB][64 tok][64]
   static constexpr int kOffQ = 0;
-  static constexpr int kOffP = kOffQ + kQBytes;
-  static constexpr int kOffKV = kOffP + 2 * kPBytes;
+  static constexpr int kOffP = kOffQ + kQBytes;     // [buffer 2][plane][128][64]
+  static constexpr int kOffKV = kOffP + 2 * kPPlanes * kPBytes;
   static constexpr int kOffBar = kOffKV + kStages * 2 * kTileBytes;
   static constexpr int kBytes = kOffBar + 1024;
   static constexpr int kAlloc = kBytes + 1024;  // manual 1024-B alignment slack
 };
 
 // barrier slots (8 B each) inside the barrier block
+constexpr int kMaxStages = 4;
 enum Bar : int {
   KV_FULL = 0,
-  KV_EMPTY = KV_FULL + kStages,
-  S_FULL = KV_EMPTY + kStages,
+  KV_EMPTY = KV_FULL + kMaxStages,
+  S_FULL = KV_EMPTY + kMaxStages,
   S_EMPTY = S_FULL + 2,
   P_FULL = S_EMPTY + 2,
   P_EMPTY = P_FULL + 2,
@@ -64,19 +69,26 @@ enum Bar : int {
   NUM_BARS = Q_EMPTY + 1
 };
 
-template <typename T> struct Fmt;
 template <> struct Fmt<__half> {
   static constexpr int ab = 0;
+  static constexpr bool kSplit = false;
   static __device__ __forceinline__ uint32_t pack(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
   }
+  static __device__ __forceinline__ uint32_t pack_lo(float, float, uint32_t) { return 0u; }
 };
 template <> struct Fmt<__nv_bfloat16> {
   static constexpr int ab = 1;
+  static constexpr bool kSplit = true;
   static __device__ __forceinline__ uint32_t pack(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ uint32_t pack_lo(float a, float b, uint32_t hi) {
+    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&hi);
+    float2 f = __bfloat1622float2(h);
+    return pack(a - f.x, b - f.y);
   }
 };
 
@@ -90,7 +102,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, DevPlan plan,
                   int var, const T* __restrict__ qg, T* __restrict__ out, float* __restrict__ part_o,
                   float* __restrict__ part_lse, float scale_log2) {
-  using L = Layout<D>;
+  using L = Layout<D, Fmt<T>::kSplit>;
+  constexpr int kStages = L::kStages;
   using namespace sm100;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -137,23 +150,34 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t g = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const Item item = items[it];
-        const int u = item.unit, h = item.kvh, p = plan.unit_pack[u];
-        const int ntok = plan.unit_ntok[u];
-        const int32_t* blist = plan.pack_blk + plan.pack_blk_off[p] + plan.unit_page0[u];
-        const int ntiles = (ntok + kN - 1) / kN;
-        for (int j = 0; j < ntiles; ++j, ++g) {
-          const int s = g % kStages;
+    // whole warp walks the items: lanes prefetch 32 block ids per load, lane 0
+    // waits on the ring and issues the TMA boxes
+    uint32_t g = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item item = items[it];
+      const int u = item.unit, h = item.kvh, p = plan.unit_pack[u];
+      const int ntok = plan.unit_ntok[u];
+      const int32_t* blist = plan.pack_blk + plan.pack_blk_off[p] + plan.unit_page0[u];
+      const int npages = (ntok + bs - 1) / bs;
+      const int ntiles = (ntok + kN - 1) / kN;
+      int base = -1024, blk_reg = 0;
+      for (int j = 0; j < ntiles; ++j, ++g) {
+        const int s = g % kStages;
+        const int rem = ntok - j * kN;
+        const int ngrp = rem >= kN ? kN / 16 : (rem + 15) / 16;
+        if (lane == 0) {
           mbar_wait(bar(KV_EMPTY + s), ((g / kStages) & 1) ^ 1);
-          const int rem = ntok - j * kN;
-          const int ngrp = rem >= kN ? kN / 16 : (rem + 15) / 16;
           mbar_expect_tx(bar(KV_FULL + s), (uint32_t)(ngrp * L::KB * 2048 * 2));
-          for (int gr = 0; gr < ngrp; ++gr) {
-            const int tok = j * kN + gr * 16;
-            const int blk = blist[tok / bs];
+        }
+        for (int gr = 0; gr < ngrp; ++gr) {
+          const int tok = j * kN + gr * 16;
+          const int pg = tok / bs;
+          if (pg >= base + 32) {
+            base = pg;
+            blk_reg = base + lane < npages ? __ldg(blist + base + lane) : 0;
+          }
+          const int blk = __shfl_sync(0xffffffffu, blk_reg, pg - base);
+          if (lane == 0) {
             const int off = tok % bs;
 #pragma unroll
             for (int kb = 0; kb < L::KB; ++kb) {
@@ -177,9 +201,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kN / 16; ++k) {
-          uint64_t a = umma_desc_sw128(sP + b * L::kPBytes + k * 32, 16, 1024);
+          const uint32_t pb = sP + (b * L::kPPlanes) * L::kPBytes + k * 32;
           uint64_t bd = umma_desc_sw128(sV(s) + k * 16 * 128, kN * 128, 1024);
-          umma_f16_ss(tO, a, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
+          umma_f16_ss(tO, umma_desc_sw128(pb, 16, 1024), bd, idesc_pv, (first && k == 0) ? 0u : 1u);
+          if constexpr (L::kPPlanes == 2) umma_f16_ss(tO, umma_desc_sw128(pb + L::kPBytes, 16, 1024), bd, idesc_pv, 1u);
         }
         umma_commit(bar(KV_EMPTY + s));
         umma_commit(bar(P_EMPTY + b));
@@ -290,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // P = exp2(s - m_ref) -> smem row t (K-major A operand of the PV MMA)
         mbar_wait(bar(P_EMPTY + b), ((gg >> 1) & 1) ^ 1);
-        const uint32_t prow = sP + b * L::kPBytes + t * 128;
+        const uint32_t prow = sP + (b * L::kPPlanes) * L::kPBytes + t * 128;
 #pragma unroll
         for (int ch = 0; ch < kN / 8; ++ch) {
           float e[8];
@@ -302,6 +327,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint4 v = make_uint4(Fmt<T>::pack(e[0], e[1]), Fmt<T>::pack(e[2], e[3]), Fmt<T>::pack(e[4], e[5]),
                                Fmt<T>::pack(e[6], e[7]));
           st_shared_v4(prow + ((ch ^ (t & 7)) << 4), v);
+          if constexpr (L::kPPlanes == 2) {
+            uint4 w = make_uint4(Fmt<T>::pack_lo(e[0], e[1], v.x), Fmt<T>::pack_lo(e[2], e[3], v.y),
+                                 Fmt<T>::pack_lo(e[4], e[5], v.z), Fmt<T>::pack_lo(e[6], e[7], v.w));
+            st_shared_v4(prow + L::kPBytes + ((ch ^ (t & 7)) << 4), w);
+          }
         }
         if (valid < kN) {
           // tail tile: zero V rows past the span (pages past the unit were not
@@ -404,7 +434,7 @@ int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t num_blocks, i
 template <int D, typename T>
 static cudaError_t launch_tc_t(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var, int grid,
                                const void* q, void* out, float* po, float* pl, float scale_log2, cudaStream_t st) {
-  constexpr int smem = tc::Layout<D>::kAlloc;
+  constexpr int smem = tc::Layout<D, tc::Fmt<T>::kSplit>::kAlloc;
   static bool init = false;
   if (!init) {
     cudaError_t e = cudaFuncSetAttribute(tc::fwd_tc_kernel<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -76,3 +76,32 @@ def test_tc_full_configs_sampled(name, nsample=4):
         ref = AO.full_attention(q[qi:qi + 1].double().cpu().numpy(), [k], [v])[0]
         for tc in outs:
             _close(outs[tc][qi].double().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("name", ["c4"])
+@pytest.mark.parametrize("tc", [64, -1])
+def test_variant_configs_vs_oracle(name, tc):
+    """Same as above, one kernel mix at a time (diagnostic granularity)."""
+    w = configs.workload(name)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    nb = w.num_pool_blocks()
+    dt = torch.bfloat16
+    kc = torch.randn(nb, w.block_size, w.num_kv_heads, w.head_dim, device="cuda", dtype=dt, generator=g)
+    vc = torch.randn(nb, w.block_size, w.num_kv_heads, w.head_dim, device="cuda", dtype=dt, generator=g)
+    q = torch.randn(w.batch, w.num_heads, w.head_dim, device="cuda", dtype=dt, generator=g) * 3
+    table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    plan = PatPlan.from_table(table, w.num_heads, w.num_kv_heads, w.head_dim, split="native", tc_min_rows=tc)
+    out = P.pat_attention(plan, q, kc, vc)
+    torch.cuda.synchronize()
+    for qi in (0, 77, 255):
+        row = w.rows[qi]
+        n = (len(row) - 1) * w.block_size + w.valid_last[qi]
+        idx = torch.tensor(row, device="cuda")
+        k = kc[idx].reshape(-1, w.num_kv_heads, w.head_dim)[:n].double().cpu().numpy()
+        v = vc[idx].reshape(-1, w.num_kv_heads, w.head_dim)[:n].double().cpu().numpy()
+        ref = AO.full_attention(q[qi:qi + 1].double().cpu().numpy(), [k], [v])[0]
+        got = out[qi].double().cpu().numpy()
+        err = np.abs(got - ref)
+        bad = err > 2e-3 + 1e-2 * np.abs(ref)
+        heads = sorted(set(np.nonzero(bad)[0].tolist()))
+        assert not bad.any(), f"q{qi}: {bad.sum()} bad, heads {heads[:16]}, max err {err.max():.3e}"
