@@ -10,7 +10,7 @@ import os
 
 from . import errors
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpatb200.so")
+LIB_PATH = os.environ.get("PAT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpatb200.so")
 
 PAT_DTYPE_F16 = 0
 PAT_DTYPE_BF16 = 1

@@ -110,12 +110,13 @@ struct StreamSmem {
   static constexpr int kTileBytes = kStageTok * D * 2;  // one K or V stage tile
   static constexpr int kStageBytes = 2 * kTileBytes;
   static constexpr int kNumStages = D == 128 ? 5 : 8;
-  static constexpr int kQBytes = WM * 16 * D * 2;
+  static constexpr int kQBytes = WM * 16 * D * 2;       // linear [rows][D] (bulk-copied)
   static constexpr int kScratchBytes = 4 * 16 * D * 4 + 2 * 4 * 16 * 4;  // epilogue: per-warp O, m, l
-  static constexpr int kOffQ = kNumStages * kStageBytes;
-  static constexpr int kOffScratch = kOffQ + kQBytes;
+  static constexpr int kOffQ = kNumStages * kStageBytes;  // two Q buffers
+  static constexpr int kOffScratch = kOffQ + 2 * kQBytes;
   static constexpr int kOffBar = kOffScratch + kScratchBytes;
-  static constexpr int kBytes = kOffBar + 2 * kNumStages * 8 + 64;
+  static constexpr int kNumBars = 2 * kNumStages + 4;
+  static constexpr int kBytes = kOffBar + kNumBars * 8;
   static constexpr int kAlloc = kBytes + 1024;
 };
 
@@ -149,13 +150,24 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* tmap, uint
       "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n)); }
 
-// Streaming forward: one TMA producer warp runs ahead through the CTA's items
-// (prefetching the next item's pages while the current one finishes), four
-// mma.sync consumer warps compute.  Stage = 64 tokens of K and V for one kv head
-// in the [16-token group][D/64][16][64] swizzled layout (one TMA box per group
-// and 64-column half).
+__device__ __forceinline__ Item load_item(const Item* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  int4 a = __ldg(q), b = __ldg(q + 1);
+  return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+}
+
+// Streaming forward: one producer warp runs ahead through the CTA's items --
+// TMA boxes for every 16-token page slice of K and V (5-stage ring) and a bulk
+// copy of the item's Q rows into a double-buffered Q tile -- while four mma.sync
+// consumer warps compute.  The producer prefetches the next item's descriptor
+// and block ids, so item boundaries never drain the ring.
 template <int WM, int D, typename T>
 __global__ void __launch_bounds__(kStreamThreads, 1)
     fwd_stream_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
@@ -168,12 +180,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   constexpr int NT = TW / 8;          // score n-tiles per warp
   constexpr int KS = D / 16;          // k-steps over head_dim
   constexpr int CH = D / 8;           // 16-byte chunks per token row
+  constexpr int ROWS = WM * 16;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t sq = sbase + S::kOffQ;
   const uint32_t full0 = sbase + S::kOffBar, empty0 = full0 + NS * 8;
+  const uint32_t qfull0 = empty0 + NS * 8, qempty0 = qfull0 + 16;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = plan.H, G = plan.G, bs = plan.bs;
@@ -185,28 +198,54 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 4);
     }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(qfull0 + 8 * b, 1);
+      mbar_init(qempty0 + 8 * b, 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
   if (warp == 4) {
-    // ------------------------------------------------------------ TMA producer
-    // The whole warp walks the items; lanes prefetch 32 block ids at a time
-    // (one coalesced load instead of a dependent load per page), lane 0 waits on
-    // the ring and issues the TMA boxes.
+    // ------------------------------------------------------------ producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmk) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmv) : "memory");
     }
-    uint32_t g = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const Item item = items[it];
-      const int u = item.unit, h = item.kvh, p = plan.unit_pack[u];
-      const int ntok = plan.unit_ntok[u];
-      const int32_t* blist = plan.pack_blk + plan.pack_blk_off[p] + plan.unit_page0[u];
+    uint32_t g = 0, n = 0;
+    int it = blockIdx.x;
+    Item item;
+    if (it < n_items) item = load_item(items + it);
+    for (; it < n_items; it += gridDim.x, ++n) {
+      const int nxt = it + gridDim.x;
+      Item next_item = item;
+      if (nxt < n_items) next_item = load_item(items + nxt);  // overlaps this item's issue
+      const int h = item.kvh, ntok = item.ntok;
+      const int32_t* blist = plan.pack_blk + item.blk;
       const int npages = (ntok + bs - 1) / bs;
       const int nst = (ntok + kStageTok - 1) / kStageTok;
-      int base = -1024, blk_reg = 0;
+      int base = 0;
+      int blk_reg = lane < npages ? __ldg(blist + lane) : 0;
+      // Q rows of this item: one bulk copy per query (its rows are contiguous heads)
+      {
+        const uint32_t qb = n & 1;
+        const uint32_t dq = sbase + S::kOffQ + qb * S::kQBytes;
+        const int r_end = item.row0 + item.nrows;
+        const int i0 = item.row0 / G, i1 = (r_end - 1) / G;
+        int myqid = 0;
+        if (lane <= i1 - i0) myqid = __ldg(plan.pack_q + item.qoff + i0 + lane);
+        if (lane == 0) {
+          mbar_wait(qempty0 + 8 * qb, ((n >> 1) & 1) ^ 1);
+          mbar_expect_tx(qfull0 + 8 * qb, (uint32_t)(item.nrows * D * 2));
+        }
+        __syncwarp();
+        for (int i = i0 + lane; i <= i1; i += 32) {
+          const int a = max(i * G, item.row0), b = min((i + 1) * G, r_end);
+          const int qid = i - i0 < 32 ? myqid : __ldg(plan.pack_q + item.qoff + i);
+          const T* src = qg + ((int64_t)qid * H + h * G + (a - i * G)) * D;
+          bulk_load(dq + (a - item.row0) * D * 2, src, (uint32_t)((b - a) * D * 2), qfull0 + 8 * qb);
+        }
+      }
       for (int st = 0; st < nst; ++st, ++g) {
         const int s = g % NS;
         const int rem = ntok - st * kStageTok;
@@ -235,43 +274,43 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           }
         }
       }
+      item = next_item;
     }
     return;
   }
 
   // -------------------------------------------------------------- consumers
   const int mt = warp / WN, wn = warp % WN;
-  uint32_t g = 0;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const Item item = items[it];
-    const int u = item.unit, h = item.kvh;
-    const int p = plan.unit_pack[u];
-    const int ntok = plan.unit_ntok[u];
-    const int qoff = plan.pack_q_off[p];
+  uint32_t g = 0, n = 0;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
+    const Item item = load_item(items + it);
+    const int h = item.kvh, ntok = item.ntok;
     const int nst = (ntok + kStageTok - 1) / kStageTok;
-
-    // ---- Q tile -> smem (rows beyond nrows are zero) ----
-    named_sync(1, 128);  // previous item's ldmatrix of Q and scratch reads are done
-    for (int c = tid; c < WM * 16 * CH; c += 128) {
-      int r = c / CH, ch = c % CH;
-      uint4 v = make_uint4(0, 0, 0, 0);
+    // epilogue metadata, prefetched now: warp w writes rows w, w+4, ...; lane k
+    // holds (qid, slot) of row w + 4k
+    int meta_qid = 0, meta_slot = -1;
+    if (lane < ROWS / 4) {
+      const int r = warp + 4 * lane;
       if (r < item.nrows) {
-        int row = item.row0 + r;
-        int qid = __ldg(plan.pack_q + qoff + row / G);
-        v = __ldg(reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + h * G + row % G) * D) + ch);
+        const int i = (item.row0 + r) / G;
+        meta_qid = __ldg(plan.pack_q + item.qoff + i);
+        meta_slot = __ldg(plan.unit_slot + item.slot_off + i);
       }
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(sq + swz_q<WM * 16>(r, ch)), "r"(v.x),
-                   "r"(v.y), "r"(v.z), "r"(v.w)
-                   : "memory");
     }
-    named_sync(1, 128);
+
+    // Q fragments (A operand) from the bulk-copied tile, then release the buffer
+    const uint32_t qb = n & 1;
+    const uint32_t sq = sbase + S::kOffQ + qb * S::kQBytes;
+    mbar_wait(qfull0 + 8 * qb, (n >> 1) & 1);
     uint32_t qa[KS][4];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       int r = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
       int ch = ks * 2 + (lane >> 4);
-      ldsm_x4(qa[ks], sq + swz_q<WM * 16>(r, ch));
+      ldsm_x4(qa[ks], sq + r * (D * 2) + ch * 16);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(qempty0 + 8 * qb);
 
     float o[D / 8][4];
 #pragma unroll
@@ -296,7 +335,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         }
         __syncwarp();
       }
-
+#ifdef PAT_STREAM_NOCOMPUTE
+      if (true) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * s);
+        continue;
+      }
+#endif
       float sc[NT][4];
 #pragma unroll
       for (int j = 0; j < NT; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
@@ -389,6 +434,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     float* so = reinterpret_cast<float*>(smem + S::kOffScratch);  // [4 warps][16][D]
     float* sm = so + 4 * 16 * D;                                  // [4][16]
     float* sl = sm + 4 * 16;                                      // [4][16]
+    named_sync(1, 128);  // previous item's scratch reads are done
     {
       const int ra = lane >> 2, rb = ra + 8, cb = 2 * (lane & 3);
       float* wo = so + warp * 16 * D;
@@ -405,11 +451,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       }
     }
     named_sync(1, 128);
-    const int* uslot = plan.unit_slot + plan.unit_slot_off[u];
-    for (int c = tid; c < WM * 16 * (D / 4); c += 128) {
-      int r = c / (D / 4), x = (c % (D / 4)) * 4;
-      if (r >= item.nrows) continue;
-      int tile = r / 16, rr = r % 16;
+#pragma unroll
+    for (int k = 0; k < ROWS / 4; ++k) {
+      const int r = warp + 4 * k;
+      const int qid = __shfl_sync(0xffffffffu, meta_qid, k);
+      const int slot = __shfl_sync(0xffffffffu, meta_slot, k);
+      if (r >= item.nrows || lane * 4 >= D) continue;
+      const int x = lane * 4;
+      const int tile = r / 16, rr = r % 16;
       float M = -INFINITY;
 #pragma unroll
       for (int w = 0; w < WN; ++w) M = fmaxf(M, sm[(tile * WN + w) * 16 + rr]);
@@ -417,21 +466,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int w = 0; w < WN; ++w) {
-        int ww = tile * WN + w;
-        float f = exp2f(sm[ww * 16 + rr] - M);
+        const int ww = tile * WN + w;
+        const float f = exp2f(sm[ww * 16 + rr] - M);
         L += sl[ww * 16 + rr] * f;
-        float4 v = *reinterpret_cast<const float4*>(so + (ww * 16 + rr) * D + x);
+        const float4 v = *reinterpret_cast<const float4*>(so + (ww * 16 + rr) * D + x);
         acc.x += v.x * f;
         acc.y += v.y * f;
         acc.z += v.z * f;
         acc.w += v.w * f;
       }
       const float inv = 1.f / L;
-      int row = item.row0 + r;
-      int i = row / G;
-      int qid = plan.pack_q[qoff + i];
-      int head = h * G + row % G;
-      int slot = uslot[i];
+      const int head = h * G + (item.row0 + r) % G;
       if (slot < 0) {
         T* dst = out + ((int64_t)qid * H + head) * D + x;
         uint2 pk;
@@ -441,7 +486,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       } else {
         float* dst = part_o + ((int64_t)slot * H + head) * D + x;
         *reinterpret_cast<float4*>(dst) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-        if (x == 0) part_lse[(int64_t)slot * H + head] = M + log2f(L);
+        if (lane == 0) part_lse[(int64_t)slot * H + head] = M + log2f(L);
       }
     }
   }

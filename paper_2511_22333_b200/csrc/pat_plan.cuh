@@ -24,12 +24,18 @@ PAT_HD int choose_variant(int rows, int tc_min_rows) {
   return rows <= 16 ? VAR_R16 : (rows <= 32 ? VAR_R32 : VAR_R64);
 }
 
-// Work item: unit, kv head, first row, row count (rows = query_in_pack * G + g).
-struct Item {
+// Work item: unit, kv head, first row, row count (rows = query_in_pack * G + g),
+// plus everything a kernel needs at item start, resolved by the scheduler so a
+// CTA issues ONE 32-byte load per item instead of a chain of dependent loads.
+struct __align__(16) Item {
   int32_t unit;
   int32_t kvh;
   int32_t row0;
   int32_t nrows;
+  int32_t blk;      // index into pack_blk of the unit's first page
+  int32_t ntok;     // tokens of the unit
+  int32_t qoff;     // index into pack_q of the pack's first query
+  int32_t slot_off; // index into unit_slot of the unit's first member
 };
 
 // Device view of a plan (all pointers are device addresses).

@@ -170,7 +170,9 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S)
     int v = choose_variant(rows, sp.tc_min_rows);
     int R = variant_rows(v);
     for (int r0 = 0; r0 < rows; r0 += R)
-      for (int h = 0; h < sp.KVH; ++h) S->items[v].push_back({u, h, r0, std::min(R, rows - r0)});
+      for (int h = 0; h < sp.KVH; ++h)
+        S->items[v].push_back({u, h, r0, std::min(R, rows - r0), P.blk_off[p] + S->unit_page0[u], S->unit_ntok[u],
+                               P.q_off[p], S->unit_slot_off[u]});
   }
   (void)unit_begin;
   return PAT_OK;
