@@ -109,7 +109,8 @@ struct StreamSmem {
   static constexpr int KB = D / 64;
   static constexpr int kTileBytes = kStageTok * D * 2;  // one K or V stage tile
   static constexpr int kStageBytes = 2 * kTileBytes;
-  static constexpr int kNumStages = D == 128 ? 5 : 8;
+  // K+V ring: as deep as the 227 KB budget allows next to Q (x2) and the scratch
+  static constexpr int kNumStages = D == 128 ? (WM == 4 ? 4 : 5) : 8;
   static constexpr int kQBytes = WM * 16 * D * 2;       // linear [rows][D] (bulk-copied)
   static constexpr int kScratchBytes = 4 * 16 * D * 4 + 2 * 4 * 16 * 4;  // epilogue: per-warp O, m, l
   static constexpr int kOffQ = kNumStages * kStageBytes;  // two Q buffers
@@ -120,7 +121,8 @@ struct StreamSmem {
   static constexpr int kAlloc = kBytes + 1024;
 };
 
-constexpr int kStreamThreads = 160;  // warps 0-3 consumers (mma.sync), warp 4 TMA producer
+// warps 0-3 consumers (mma.sync), warp 4 producer (one thread)
+constexpr int kStreamThreads = 160;
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
@@ -208,10 +210,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 
   if (warp == 4) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmk) : "memory");
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmv) : "memory");
-    }
+    // One thread: item descriptors one item ahead, block ids one stage ahead
+    // (independent loads, latency hidden behind the ring wait), Q rows by bulk
+    // copy, K/V page slices by TMA.
+    if (lane != 0) return;
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmk) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmv) : "memory");
     uint32_t g = 0, n = 0;
     int it = blockIdx.x;
     Item item;
@@ -219,58 +223,61 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     for (; it < n_items; it += gridDim.x, ++n) {
       const int nxt = it + gridDim.x;
       Item next_item = item;
-      if (nxt < n_items) next_item = load_item(items + nxt);  // overlaps this item's issue
+      if (nxt < n_items) next_item = load_item(items + nxt);
       const int h = item.kvh, ntok = item.ntok;
       const int32_t* blist = plan.pack_blk + item.blk;
-      const int npages = (ntok + bs - 1) / bs;
       const int nst = (ntok + kStageTok - 1) / kStageTok;
-      int base = 0;
-      int blk_reg = lane < npages ? __ldg(blist + lane) : 0;
-      // Q rows of this item: one bulk copy per query (its rows are contiguous heads)
+      auto stage_ids = [&](int st, int* b4) {
+#pragma unroll
+        for (int gr = 0; gr < 4; ++gr) {
+          const int tok = st * kStageTok + gr * 16;
+          b4[gr] = tok < ntok ? __ldg(blist + tok / bs) : 0;
+        }
+      };
+#if !(defined(PAT_STREAM_NOCOMPUTE) && PAT_STREAM_NOCOMPUTE >= 2)
       {
         const uint32_t qb = n & 1;
         const uint32_t dq = sbase + S::kOffQ + qb * S::kQBytes;
         const int r_end = item.row0 + item.nrows;
         const int i0 = item.row0 / G, i1 = (r_end - 1) / G;
-        int myqid = 0;
-        if (lane <= i1 - i0) myqid = __ldg(plan.pack_q + item.qoff + i0 + lane);
-        if (lane == 0) {
-          mbar_wait(qempty0 + 8 * qb, ((n >> 1) & 1) ^ 1);
-          mbar_expect_tx(qfull0 + 8 * qb, (uint32_t)(item.nrows * D * 2));
-        }
-        __syncwarp();
-        for (int i = i0 + lane; i <= i1; i += 32) {
-          const int a = max(i * G, item.row0), b = min((i + 1) * G, r_end);
-          const int qid = i - i0 < 32 ? myqid : __ldg(plan.pack_q + item.qoff + i);
+        mbar_wait(qempty0 + 8 * qb, ((n >> 1) & 1) ^ 1);
+        mbar_expect_tx(qfull0 + 8 * qb, (uint32_t)(item.nrows * D * 2));
+        for (int i = i0; i <= i1; ++i) {
+          const int a = max(i * G, item.row0), e = min((i + 1) * G, r_end);
+          const int qid = __ldg(plan.pack_q + item.qoff + i);
           const T* src = qg + ((int64_t)qid * H + h * G + (a - i * G)) * D;
-          bulk_load(dq + (a - item.row0) * D * 2, src, (uint32_t)((b - a) * D * 2), qfull0 + 8 * qb);
+          bulk_load(dq + (a - item.row0) * D * 2, src, (uint32_t)((e - a) * D * 2), qfull0 + 8 * qb);
         }
       }
+#endif
       for (int st = 0; st < nst; ++st, ++g) {
         const int s = g % NS;
         const int rem = ntok - st * kStageTok;
         const int ngrp = rem >= kStageTok ? kStageTok / 16 : (rem + 15) / 16;
         const uint32_t dk = sbase + s * S::kStageBytes, dv = dk + S::kTileBytes;
-        if (lane == 0) {
-          mbar_wait(empty0 + 8 * s, ((g / NS) & 1) ^ 1);
-          mbar_expect_tx(full0 + 8 * s, (uint32_t)(ngrp * S::KB * 2048 * 2));
-        }
+        mbar_wait(empty0 + 8 * s, ((g / NS) & 1) ^ 1);
+        mbar_expect_tx(full0 + 8 * s, (uint32_t)(ngrp * S::KB * 2048 * 2));
+#ifdef PAT_PRODUCER_BURST
+        int b4[4];
+        stage_ids(st, b4);
+#endif
         for (int gr = 0; gr < ngrp; ++gr) {
           const int tok = st * kStageTok + gr * 16;
-          const int pg = tok / bs;
-          if (pg >= base + 32) {  // warp-uniform refill of the block-id window
-            base = pg;
-            blk_reg = base + lane < npages ? __ldg(blist + base + lane) : 0;
-          }
-          const int blk = __shfl_sync(0xffffffffu, blk_reg, pg - base);
-          if (lane == 0) {
-            const int off = tok % bs;
+          // Dependent id load per page slice: the load latency paces the TMA
+          // issue, which measured faster than issuing a stage's 16 boxes as a
+          // burst (tools/kv_stream_probe.cu, profiles/).
+#ifdef PAT_PRODUCER_BURST
+          const int blk = b4[gr];
+#else
+          const int pg = bs == 16 ? (tok >> 4) : tok / bs;
+          const int blk = __ldg(blist + pg);
+#endif
+          const int off = bs == 16 ? 0 : tok - pg * bs;
 #pragma unroll
-            for (int kb = 0; kb < S::KB; ++kb) {
-              const uint32_t o = (uint32_t)((gr * S::KB + kb) * 2048);
-              tma_load_4d(dk + o, &tmk, full0 + 8 * s, kb * 64, h, off, blk);
-              tma_load_4d(dv + o, &tmv, full0 + 8 * s, kb * 64, h, off, blk);
-            }
+          for (int kb = 0; kb < S::KB; ++kb) {
+            const uint32_t o = (uint32_t)((gr * S::KB + kb) * 2048);
+            tma_load_4d(dk + o, &tmk, full0 + 8 * s, kb * 64, h, off, blk);
+            tma_load_4d(dv + o, &tmv, full0 + 8 * s, kb * 64, h, off, blk);
           }
         }
       }
@@ -281,26 +288,47 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 
   // -------------------------------------------------------------- consumers
   const int mt = warp / WN, wn = warp % WN;
-  uint32_t g = 0, n = 0;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
-    const Item item = load_item(items + it);
-    const int h = item.kvh, ntok = item.ntok;
-    const int nst = (ntok + kStageTok - 1) / kStageTok;
-    // epilogue metadata, prefetched now: warp w writes rows w, w+4, ...; lane k
-    // holds (qid, slot) of row w + 4k
-    int meta_qid = 0, meta_slot = -1;
+  // epilogue metadata: warp w writes rows w, w+4, ...; lane k holds (qid, slot)
+  // of row w + 4k.  Loaded one item ahead so item boundaries cost no latency.
+  auto load_meta = [&](const Item& itm, int& mq, int& ms) {
+    mq = 0;
+    ms = -1;
     if (lane < ROWS / 4) {
       const int r = warp + 4 * lane;
-      if (r < item.nrows) {
-        const int i = (item.row0 + r) / G;
-        meta_qid = __ldg(plan.pack_q + item.qoff + i);
-        meta_slot = __ldg(plan.unit_slot + item.slot_off + i);
+      if (r < itm.nrows) {
+        const int i = (itm.row0 + r) / G;
+        mq = __ldg(plan.pack_q + itm.qoff + i);
+        ms = __ldg(plan.unit_slot + itm.slot_off + i);
       }
     }
+  };
+  uint32_t g = 0, n = 0;
+  Item item;
+  int meta_qid = 0, meta_slot = -1;
+  if ((int)blockIdx.x < n_items) {
+    item = load_item(items + blockIdx.x);
+    load_meta(item, meta_qid, meta_slot);
+  }
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
+    const int nxt = it + gridDim.x;
+    Item next_item = item;
+    if (nxt < n_items) next_item = load_item(items + nxt);
+    const int h = item.kvh, ntok = item.ntok;
+    const int nst = (ntok + kStageTok - 1) / kStageTok;
 
     // Q fragments (A operand) from the bulk-copied tile, then release the buffer
     const uint32_t qb = n & 1;
     const uint32_t sq = sbase + S::kOffQ + qb * S::kQBytes;
+#if defined(PAT_STREAM_NOCOMPUTE) && PAT_STREAM_NOCOMPUTE >= 2
+    for (int st = 0; st < nst; ++st, ++g) {
+      const int s = g % NS;
+      mbar_wait(full0 + 8 * s, (g / NS) & 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * s);
+    }
+    item = next_item;
+    continue;
+#endif
     mbar_wait(qfull0 + 8 * qb, (n >> 1) & 1);
     uint32_t qa[KS][4];
 #pragma unroll
@@ -431,6 +459,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
       lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
     }
+    int next_qid = 0, next_slot = -1;
+    if (nxt < n_items) load_meta(next_item, next_qid, next_slot);  // overlaps the epilogue
     float* so = reinterpret_cast<float*>(smem + S::kOffScratch);  // [4 warps][16][D]
     float* sm = so + 4 * 16 * D;                                  // [4][16]
     float* sl = sm + 4 * 16;                                      // [4][16]
@@ -489,6 +519,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         if (lane == 0) part_lse[(int64_t)slot * H + head] = M + log2f(L);
       }
     }
+    item = next_item;
+    meta_qid = next_qid;
+    meta_slot = next_slot;
   }
 }
 

@@ -160,8 +160,15 @@ int main() {
   uint16_t *kc, *vc;
   CK(cudaMalloc(&kc, elems * 2));
   CK(cudaMalloc(&vc, elems * 2));
-  CK(cudaMemset(kc, 0, elems * 2));
-  CK(cudaMemset(vc, 0, elems * 2));
+  {
+    // random bf16 bit patterns (finite): a zero-filled cache streams faster than real data
+    std::vector<uint16_t> h(elems);
+    std::mt19937 rng(1);
+    for (size_t i = 0; i < elems; ++i) h[i] = (uint16_t)((rng() & 0x7fff) | 0x3c00) & 0xbfff;
+    CK(cudaMemcpy(kc, h.data(), elems * 2, cudaMemcpyHostToDevice));
+    for (size_t i = 0; i < elems; ++i) h[i] = (uint16_t)((rng() & 0x7fff) | 0x3c00) & 0xbfff;
+    CK(cudaMemcpy(vc, h.data(), elems * 2, cudaMemcpyHostToDevice));
+  }
   std::vector<int> blocks(NB);
   for (int i = 0; i < NB; ++i) blocks[i] = i;
   int* dblk;
@@ -177,8 +184,9 @@ int main() {
     cuuint64_t dims[4] = {D, KVH, BS, (cuuint64_t)NB};
     cuuint64_t str[3] = {D * 2, KVH * D * 2, BS * KVH * D * 2};
     cuuint32_t box[4] = {64, 1, 16, 1}, es[4] = {1, 1, 1, 1};
-    E(&m4k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, kc, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    E(&m4v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, vc, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUtensorMapL2promotion prom = getenv("PROMO") ? (CUtensorMapL2promotion)atoi(getenv("PROMO")) : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    E(&m4k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, kc, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    E(&m4v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, vc, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   auto mk5 = [&](CUtensorMap* m, void* base, int hpc) {
     // dims: d_lo(64), tok(16), d_hi(2), head(KVH), block
