@@ -1,0 +1,461 @@
+// Tensor-core (tcgen05 + TMEM + TMA) forward kernel for WIDE packs, two
+// 128-row query tiles per CTA (FA4-style ping-pong).
+//
+// A pack whose query tile (queries x G heads of one kv head) fills >= 64 rows
+// forms a real dense contraction: S = Q K^T and O += P V run on the 5th-gen
+// tensor cores.  One CTA (12 warps, one per SM) owns work items of
+// (unit, kv head, 256 rows) = tiles A (rows 0-127) and B (rows 128-255) and
+// streams the unit's KV span ONCE for both:
+//   warp 0      TMA producer: 16-token page slices of K and V, 5-stage ring of
+//               64-token stages, 128B swizzle, from the paged cache;
+//   warp 1      MMA issuer (one thread), per KV tile j:
+//                 S_A(j) = Q_A K_j^T, S_B(j) = Q_B K_j^T   (SS, M=128 N=64 K=d)
+//                 O_A += P_A(j-1) V_{j-1}, O_B += P_B(j-1) V_{j-1}
+//                 (TS: P read straight from TMEM, V an MN-major smem operand)
+//               so the tensor core works on one tile while the other tile's
+//               softmax runs;
+//   warp 2      TMEM allocator (512 columns: S_A x2, S_B x2, O_A, O_B);
+//   warps 4-7   softmax / epilogue of tile A (thread = row = TMEM lane);
+//   warps 8-11  softmax / epilogue of tile B.
+// Softmax: tcgen05.ld S, scale/mask in log2 units, lazy O rescale (only when the
+// running max grows by > 8), P packed to 16-bit and tcgen05.st back over S
+// (bf16: P = hi + lo, two PV MMAs, ~16-bit P).  Numerics follow cta_partial
+// (attention.py:140-163): fp32 scores and accumulators.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include "pat_plan.cuh"
+#include "pat_sm100.cuh"
+
+namespace pat {
+namespace tc2 {
+
+constexpr int kThreads = 384;
+constexpr int kM = 128;       // rows per tile
+constexpr int kN = 64;        // tokens per KV tile
+constexpr int kStages = 5;
+constexpr uint32_t kTmemCols = 512;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int D>
+struct Layout {
+  static constexpr int KB = D / 64;
+  static constexpr int kQBytes = KB * kM * 128;      // one tile's Q: [KB][128][64]
+  static constexpr int kTileBytes = KB * kN * 128;   // K or V stage tile: [KB][64][64]
+  static constexpr int kOffQ = 0;                    // Q_A, Q_B
+  static constexpr int kOffKV = 2 * kQBytes;
+  static constexpr int kOffBar = kOffKV + kStages * 2 * kTileBytes;
+  static constexpr int kBytes = kOffBar + 512;
+  static constexpr int kAlloc = kBytes + 1024;
+};
+
+enum Bar : int {
+  KV_FULL = 0,
+  KV_EMPTY = KV_FULL + kStages,
+  S_FULL = KV_EMPTY + kStages,  // [tile][buf]
+  P_FULL = S_FULL + 4,          // [tile][buf]
+  O_DONE = P_FULL + 4,          // [tile]
+  O_EMPTY = O_DONE + 2,         // [tile]
+  Q_FULL = O_EMPTY + 2,         // [tile]
+  Q_EMPTY = Q_FULL + 2,         // [tile]
+  NUM_BARS = Q_EMPTY + 2
+};
+
+template <typename T> struct Fmt;
+template <> struct Fmt<__half> {
+  static constexpr int ab = 0;
+  static constexpr bool kSplit = false;
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ uint32_t pack_lo(float, float, uint32_t) { return 0u; }
+};
+template <> struct Fmt<__nv_bfloat16> {
+  static constexpr int ab = 1;
+  static constexpr bool kSplit = true;
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ uint32_t pack_lo(float a, float b, uint32_t hi) {
+    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&hi);
+    float2 f = __bfloat1622float2(h);
+    return pack(a - f.x, b - f.y);
+  }
+};
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ Item load_item(const Item* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  int4 a = __ldg(q), b = __ldg(q + 1);
+  return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+}
+
+template <int D, typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, DevPlan plan,
+                   int var, const T* __restrict__ qg, T* __restrict__ out, float* __restrict__ part_o,
+                   float* __restrict__ part_lse, float scale_log2) {
+  using L = Layout<D>;
+  using namespace sm100;
+  constexpr bool kSplit = Fmt<T>::kSplit;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t sKV = sb + L::kOffKV;
+  const uint32_t bars = sb + L::kOffBar;
+  uint32_t* tmem_slot = (uint32_t*)(smem + L::kOffBar + NUM_BARS * 8);
+  auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
+  auto sQ = [&](int x) { return sb + L::kOffQ + (uint32_t)(x * L::kQBytes); };
+  auto sK = [&](int s) { return sKV + (uint32_t)(s * 2 * L::kTileBytes); };
+  auto sV = [&](int s) { return sKV + (uint32_t)(s * 2 * L::kTileBytes + L::kTileBytes); };
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int H = plan.H, G = plan.G, bs = plan.bs;
+  const int n_items = plan.n_items[var];
+  const Item* items = plan.items[var];
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(bar(KV_FULL + s), 1);
+      mbar_init(bar(KV_EMPTY + s), 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(bar(S_FULL + i), 1);
+      mbar_init(bar(P_FULL + i), 4);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(bar(O_DONE + x), 1);
+      mbar_init(bar(O_EMPTY + x), 4);
+      mbar_init(bar(Q_FULL + x), 4);
+      mbar_init(bar(Q_EMPTY + x), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S[x][b] at 64*(2x+b), O[x] at 256 + 128x
+  auto tS = [&](int x, int b) { return tmem + (uint32_t)(64 * (2 * x + b)); };
+  auto tO = [&](int x) { return tmem + 256u + (uint32_t)(128 * x); };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (one thread)
+    if (lane == 0) {
+      tma_prefetch(&tmk);
+      tma_prefetch(&tmv);
+      uint32_t g = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item item = load_item(items + it);
+        const int h = item.kvh, ntok = item.ntok;
+        const int32_t* blist = plan.pack_blk + item.blk;
+        const int ntiles = (ntok + kN - 1) / kN;
+        for (int j = 0; j < ntiles; ++j, ++g) {
+          const int s = g % kStages;
+          const int rem = ntok - j * kN;
+          const int ngrp = rem >= kN ? kN / 16 : (rem + 15) / 16;
+          mbar_wait(bar(KV_EMPTY + s), ((g / kStages) & 1) ^ 1);
+          mbar_expect_tx(bar(KV_FULL + s), (uint32_t)(ngrp * L::KB * 2048 * 2));
+          for (int gr = 0; gr < ngrp; ++gr) {
+            const int tok = j * kN + gr * 16;
+            const int pg = bs == 16 ? (tok >> 4) : tok / bs;
+            const int blk = __ldg(blist + pg);
+            const int off = bs == 16 ? 0 : tok - pg * bs;
+#pragma unroll
+            for (int kb = 0; kb < L::KB; ++kb) {
+              tma_load_4d(sK(s) + kb * (kN * 128) + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
+              tma_load_4d(sV(s) + kb * (kN * 128) + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
+      constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
+      uint32_t g = 0;           // KV tiles consumed
+      uint32_t c[2] = {0, 0};   // KV tiles processed per query tile (S/P buffer index)
+      uint32_t ni[2] = {0, 0};  // items processed per query tile
+      auto issue_qk = [&](int x, int s, uint32_t ci) {
+        const int b = ci & 1;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const int kb = k >> 2, kk = k & 3;
+          uint64_t a = umma_desc_sw128(sQ(x) + kb * (kM * 128) + kk * 32, 16, 1024);
+          uint64_t bd = umma_desc_sw128(sK(s) + kb * (kN * 128) + kk * 32, 16, 1024);
+          umma_f16_ss(tS(x, b), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+        }
+        umma_commit(bar(S_FULL + 2 * x + b));
+      };
+      auto issue_pv = [&](int x, int s, uint32_t ci, bool first) {
+        const int b = ci & 1;
+        if (first) mbar_wait(bar(O_EMPTY + x), (ni[x] & 1) ^ 1);
+        mbar_wait(bar(P_FULL + 2 * x + b), (ci >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kN / 16; ++k) {
+          uint64_t bd = umma_desc_sw128(sV(s) + k * 16 * 128, kN * 128, 1024);
+          // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
+          umma_f16_ts(tO(x), tS(x, b) + k * 8, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
+          if constexpr (kSplit) umma_f16_ts(tO(x), tS(x, b) + 32 + k * 8, bd, idesc_pv, 1u);
+        }
+        umma_commit(bar(O_DONE + x));
+      };
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item item = load_item(items + it);
+        const bool liveB = item.nrows > kM;
+        const int ntiles = (item.ntok + kN - 1) / kN;
+        mbar_wait(bar(Q_FULL + 0), ni[0] & 1);
+        if (liveB) mbar_wait(bar(Q_FULL + 1), ni[1] & 1);
+        tc_fence_after();
+        int sprev = 0;
+        for (int j = 0; j < ntiles; ++j, ++g) {
+          const int s = g % kStages;
+          mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
+          tc_fence_after();
+          issue_qk(0, s, c[0] + j);
+          if (liveB) issue_qk(1, s, c[1] + j);
+          if (j == ntiles - 1) {
+            umma_commit(bar(Q_EMPTY + 0));
+            if (liveB) umma_commit(bar(Q_EMPTY + 1));
+          }
+          if (j > 0) {
+            issue_pv(0, sprev, c[0] + j - 1, j == 1);
+            if (liveB) issue_pv(1, sprev, c[1] + j - 1, j == 1);
+            umma_commit(bar(KV_EMPTY + sprev));
+          }
+          sprev = s;
+        }
+        issue_pv(0, sprev, c[0] + ntiles - 1, ntiles == 1);
+        if (liveB) issue_pv(1, sprev, c[1] + ntiles - 1, ntiles == 1);
+        umma_commit(bar(KV_EMPTY + sprev));
+        c[0] += ntiles;
+        ++ni[0];
+        if (liveB) {
+          c[1] += ntiles;
+          ++ni[1];
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax / epilogue
+    const int x = (warp - 4) >> 2;       // query tile
+    const int t = tid - 128 - x * 128;   // row in the tile == TMEM lane
+    const int wg = (warp - 4) & 3;       // lane quarter
+    const uint32_t lane_base = (uint32_t)(wg * 32) << 16;
+    uint32_t c = 0, ni = 0, g = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item item = load_item(items + it);
+      const int ntok = item.ntok;
+      const int ntiles = (ntok + kN - 1) / kN;
+      if (x == 1 && item.nrows <= kM) {
+        g += ntiles;
+        continue;  // tile B idle for this item
+      }
+      const int h = item.kvh;
+      const int r = x * kM + t;  // row within the item
+      const bool live = r < item.nrows;
+      const int row = item.row0 + r;
+      const int qi = live ? row / G : 0;
+      const int qid = live ? __ldg(plan.pack_q + item.qoff + qi) : 0;
+      const int head = h * G + (live ? row % G : 0);
+      const int slot = live ? __ldg(plan.unit_slot + item.slot_off + qi) : -1;
+
+      // Q row -> smem (after the previous item's last QK of this tile)
+      mbar_wait(bar(Q_EMPTY + x), (ni & 1) ^ 1);
+      {
+        const uint4* src = reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + head) * D);
+#pragma unroll
+        for (int ch = 0; ch < D / 8; ++ch) {
+          uint4 v = live ? __ldg(src + ch) : make_uint4(0, 0, 0, 0);
+          st_shared_v4(sQ(x) + (ch >> 3) * (kM * 128) + t * 128 + (((ch & 7) ^ (t & 7)) << 4), v);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(Q_FULL + x));
+
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < ntiles; ++j, ++c, ++g) {
+        const int b = c & 1;
+        mbar_wait(bar(S_FULL + 2 * x + b), (c >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[kN];
+        tmem_ld32(tS(x, b) + lane_base, sr);
+        tmem_ld32(tS(x, b) + lane_base + 32, sr + 32);
+        tmem_wait_ld();
+
+        const int valid = ntok - j * kN;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < kN; ++k) {
+          float v = k < valid ? __uint_as_float(sr[k]) * scale_log2 : -INFINITY;
+          sr[k] = __float_as_uint(v);
+          mx = fmaxf(mx, v);
+        }
+        const bool need = mx > m_ref + kRescaleThreshold;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m_new = need ? mx : m_ref;
+          const float alpha = exp2f(m_ref - m_new);
+          if (j > 0) {
+            mbar_wait(bar(O_DONE + x), (c - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int q = 0; q < D / 32; ++q) {
+              uint32_t o[32];
+              tmem_ld32(tO(x) + lane_base + q * 32, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              tmem_st32(tO(x) + lane_base + q * 32, o);
+            }
+          }
+          l *= alpha;
+          m_ref = m_new;
+        }
+        // P = exp2(s - m_ref), packed 16-bit pairs, stored over S (hi: cols 0-31, lo: 32-63)
+        uint32_t ph[kN / 2], pl[kN / 2];
+#pragma unroll
+        for (int k = 0; k < kN / 2; ++k) {
+          const float e0 = exp2f(__uint_as_float(sr[2 * k]) - m_ref);
+          const float e1 = exp2f(__uint_as_float(sr[2 * k + 1]) - m_ref);
+          l += e0 + e1;
+          ph[k] = Fmt<T>::pack(e0, e1);
+          if constexpr (kSplit) pl[k] = Fmt<T>::pack_lo(e0, e1, ph[k]);
+        }
+        tmem_st32(tS(x, b) + lane_base, ph);
+        if constexpr (kSplit) tmem_st32(tS(x, b) + lane_base + 32, pl);
+        if (valid < kN) {
+          // tail tile: zero V rows past the span (both tiles may do it: same zeros)
+          const int s = g % kStages;
+          mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
+          const int nz = (kN - valid) * L::KB * 8;
+          for (int q = t; q < nz; q += 128) {
+            const int rr = valid + q / (L::KB * 8);
+            const int kb = (q / 8) % L::KB, ch = q % 8;
+            st_shared_v4(sV(s) + kb * (kN * 128) + rr * 128 + (ch << 4), make_uint4(0, 0, 0, 0));
+          }
+          fence_proxy_async_smem();
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(P_FULL + 2 * x + b));
+      }
+
+      // epilogue: O / l
+      mbar_wait(bar(O_DONE + x), (c - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+#pragma unroll
+      for (int q = 0; q < D / 32; ++q) {
+        uint32_t o[32];
+        tmem_ld32(tO(x) + lane_base + q * 32, o);
+        tmem_wait_ld();
+        if (live) {
+          if (slot < 0) {
+            uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)qid * H + head) * D + q * 32);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float* f = reinterpret_cast<const float*>(o + k * 8);
+              dst[k] = make_uint4(Fmt<T>::pack(f[0] * inv, f[1] * inv), Fmt<T>::pack(f[2] * inv, f[3] * inv),
+                                  Fmt<T>::pack(f[4] * inv, f[5] * inv), Fmt<T>::pack(f[6] * inv, f[7] * inv));
+            }
+          } else {
+            float4* dst = reinterpret_cast<float4*>(part_o + ((int64_t)slot * H + head) * D + q * 32);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float* f = reinterpret_cast<const float*>(o + k * 4);
+              dst[k] = make_float4(f[0] * inv, f[1] * inv, f[2] * inv, f[3] * inv);
+            }
+          }
+        }
+      }
+      if (live && slot >= 0) part_lse[(int64_t)slot * H + head] = m_ref + log2f(l);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(O_EMPTY + x));
+      ++ni;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+}  // namespace tc2
+
+// ------------------------------------------------------------------------------------------
+// host side: TMA descriptors over the paged cache + launch
+// ------------------------------------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 4-D map over a paged cache [num_blocks][bs][KVH][D]: box (64 d, 1 head, 16 tokens, 1 block).
+int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t num_blocks, int bs, int kvh, int d, int dtype) {
+  auto enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)kvh, (cuuint64_t)bs, (cuuint64_t)num_blocks};
+  cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)kvh * d * 2, (cuuint64_t)bs * kvh * d * 2};
+  cuuint32_t box[4] = {64, 1, 16, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, dtype == PAT_DTYPE_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+
+template <int D, typename T>
+static cudaError_t launch_tc2_t(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var,
+                                int grid, const void* q, void* out, float* po, float* pl, float scale_log2,
+                                cudaStream_t st) {
+  constexpr int smem = tc2::Layout<D>::kAlloc;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(tc2::fwd_tc2_kernel<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  tc2::fwd_tc2_kernel<D, T><<<grid, tc2::kThreads, smem, st>>>(tmk, tmv, plan, var, (const T*)q, (T*)out, po, pl,
+                                                               scale_log2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_forward_tc(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var, int grid,
+                              int dtype, int d, const void* q, void* out, float* po, float* pl, float scale_log2,
+                              cudaStream_t st) {
+  if (dtype == PAT_DTYPE_F16) {
+    if (d == 128) return launch_tc2_t<128, __half>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
+    return launch_tc2_t<64, __half>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
+  }
+  if (d == 128) return launch_tc2_t<128, __nv_bfloat16>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
+  return launch_tc2_t<64, __nv_bfloat16>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
+}
+
+}  // namespace pat
