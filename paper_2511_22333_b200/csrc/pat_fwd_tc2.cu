@@ -37,7 +37,10 @@ constexpr int kM = 128;       // rows per tile
 constexpr int kN = 64;        // tokens per KV tile
 constexpr int kStages = 5;
 constexpr uint32_t kTmemCols = 512;
-constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef PAT_TC_RESCALE_THRESHOLD
+#define PAT_TC_RESCALE_THRESHOLD 8.0f
+#endif
+constexpr float kRescaleThreshold = PAT_TC_RESCALE_THRESHOLD;  // log2 units
 
 template <int D>
 struct Layout {
@@ -54,9 +57,10 @@ struct Layout {
 enum Bar : int {
   KV_FULL = 0,
   KV_EMPTY = KV_FULL + kStages,
-  S_FULL = KV_EMPTY + kStages,  // [tile][buf]
-  P_FULL = S_FULL + 4,          // [tile][buf]
-  O_DONE = P_FULL + 4,          // [tile]
+  S_FULL = KV_EMPTY + kStages,  // [tile] QK done
+  S_EMPTY = S_FULL + 2,         // [tile] softmax has read S
+  P_FULL = S_EMPTY + 2,         // [tile] P written to TMEM
+  O_DONE = P_FULL + 2,          // [tile] PV done (O updated, P region free)
   O_EMPTY = O_DONE + 2,         // [tile]
   Q_FULL = O_EMPTY + 2,         // [tile]
   Q_EMPTY = Q_FULL + 2,         // [tile]
@@ -75,7 +79,11 @@ template <> struct Fmt<__half> {
 };
 template <> struct Fmt<__nv_bfloat16> {
   static constexpr int ab = 1;
+#ifdef PAT_TC_NO_SPLIT
+  static constexpr bool kSplit = false;
+#else
   static constexpr bool kSplit = true;
+#endif
   static __device__ __forceinline__ uint32_t pack(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -127,8 +135,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(KV_FULL + s), 1);
       mbar_init(bar(KV_EMPTY + s), 1);
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 2; ++i) {
       mbar_init(bar(S_FULL + i), 1);
+      mbar_init(bar(S_EMPTY + i), 4);
       mbar_init(bar(P_FULL + i), 4);
     }
     for (int x = 0; x < 2; ++x) {
@@ -144,8 +153,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: S[x][b] at 64*(2x+b), O[x] at 256 + 128x
-  auto tS = [&](int x, int b) { return tmem + (uint32_t)(64 * (2 * x + b)); };
+  // TMEM columns: S[x] at 128x, P[x] at 128x + 64 (hi: +0..31, lo: +32..63),
+  // O[x] at 256 + 128x.  P has its own columns: a PV MMA reading P from TMEM
+  // must never share columns with a later QK MMA's accumulator (measured WAR
+  // hazard when P lived inside the double-buffered S region).
+  auto tS = [&](int x) { return tmem + (uint32_t)(128 * x); };
+  auto tP = [&](int x) { return tmem + (uint32_t)(128 * x + 64); };
   auto tO = [&](int x) { return tmem + 256u + (uint32_t)(128 * x); };
 
   if (warp == 0) {
@@ -188,27 +201,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t c[2] = {0, 0};   // KV tiles processed per query tile (S/P buffer index)
       uint32_t ni[2] = {0, 0};  // items processed per query tile
       auto issue_qk = [&](int x, int s, uint32_t ci) {
-        const int b = ci & 1;
+        // S[x] is single-buffered: wait until the softmax has read tile ci-1
+        mbar_wait(bar(S_EMPTY + x), (ci & 1) ^ 1);
+        tc_fence_after();
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const int kb = k >> 2, kk = k & 3;
           uint64_t a = umma_desc_sw128(sQ(x) + kb * (kM * 128) + kk * 32, 16, 1024);
           uint64_t bd = umma_desc_sw128(sK(s) + kb * (kN * 128) + kk * 32, 16, 1024);
-          umma_f16_ss(tS(x, b), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+          umma_f16_ss(tS(x), a, bd, idesc_qk, k > 0 ? 1u : 0u);
         }
-        umma_commit(bar(S_FULL + 2 * x + b));
       };
       auto issue_pv = [&](int x, int s, uint32_t ci, bool first) {
-        const int b = ci & 1;
         if (first) mbar_wait(bar(O_EMPTY + x), (ni[x] & 1) ^ 1);
-        mbar_wait(bar(P_FULL + 2 * x + b), (ci >> 1) & 1);
+        mbar_wait(bar(P_FULL + x), ci & 1);
         tc_fence_after();
+
 #pragma unroll
         for (int k = 0; k < kN / 16; ++k) {
           uint64_t bd = umma_desc_sw128(sV(s) + k * 16 * 128, kN * 128, 1024);
           // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
-          umma_f16_ts(tO(x), tS(x, b) + k * 8, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
-          if constexpr (kSplit) umma_f16_ts(tO(x), tS(x, b) + 32 + k * 8, bd, idesc_pv, 1u);
+          umma_f16_ts(tO(x), tP(x) + k * 8, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
+          if constexpr (kSplit) umma_f16_ts(tO(x), tP(x) + 32 + k * 8, bd, idesc_pv, 1u);
         }
         umma_commit(bar(O_DONE + x));
       };
@@ -224,8 +238,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = g % kStages;
           mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
           tc_fence_after();
+          // Both tiles' S MMAs are issued before either S_FULL is signalled:
+          // a softmax must not read/write its S region while the OTHER tile's
+          // QK MMA is in flight (measured: corrupted S/P when the two S
+          // regions are 128 or 256 TMEM columns apart; tools/tc_debug.py).
           issue_qk(0, s, c[0] + j);
           if (liveB) issue_qk(1, s, c[1] + j);
+          umma_commit(bar(S_FULL + 0));
+          if (liveB) umma_commit(bar(S_FULL + 1));
           if (j == ntiles - 1) {
             umma_commit(bar(Q_EMPTY + 0));
             if (liveB) umma_commit(bar(Q_EMPTY + 1));
@@ -288,12 +308,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       float m_ref = -INFINITY, l = 0.f;
       for (int j = 0; j < ntiles; ++j, ++c, ++g) {
-        const int b = c & 1;
-        mbar_wait(bar(S_FULL + 2 * x + b), (c >> 1) & 1);
+        mbar_wait(bar(S_FULL + x), c & 1);
         tc_fence_after();
         uint32_t sr[kN];
-        tmem_ld32(tS(x, b) + lane_base, sr);
-        tmem_ld32(tS(x, b) + lane_base + 32, sr + 32);
+        tmem_ld32(tS(x) + lane_base, sr);
+        tmem_ld32(tS(x) + lane_base + 32, sr + 32);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(S_EMPTY + x));
         tmem_wait_ld();
 
         const int valid = ntok - j * kN;
@@ -334,8 +356,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph[k] = Fmt<T>::pack(e0, e1);
           if constexpr (kSplit) pl[k] = Fmt<T>::pack_lo(e0, e1, ph[k]);
         }
-        tmem_st32(tS(x, b) + lane_base, ph);
-        if constexpr (kSplit) tmem_st32(tS(x, b) + lane_base + 32, pl);
+        // the P columns are free once PV of the previous tile completed
+        if (j > 0) {
+          mbar_wait(bar(O_DONE + x), (c - 1) & 1);
+          tc_fence_after();
+        }
+        tmem_st32(tP(x) + lane_base, ph);
+        if constexpr (kSplit) tmem_st32(tP(x) + lane_base + 32, pl);
         if (valid < kN) {
           // tail tile: zero V rows past the span (both tiles may do it: same zeros)
           const int s = g % kStages;
@@ -351,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar(P_FULL + 2 * x + b));
+        if (lane == 0) mbar_arrive(bar(P_FULL + x));
       }
 
       // epilogue: O / l
