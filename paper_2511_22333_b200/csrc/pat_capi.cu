@@ -394,12 +394,20 @@ int pat_forward(const pat_plan* Pc, const void* q, const void* k_cache, const vo
     P->tm_blocks = num_pool_blocks;
     P->tm_dtype = dtype;
   }
+  // Concurrent variants get disjoint SM shares proportional to their estimated
+  // work (every forward kernel is persistent with one CTA per SM, and the
+  // tcgen05 and streaming CTAs cannot share an SM's shared memory).
+  double wsum = 0;
+  for (int i = 0; i < na; ++i) wsum += P->sched.work[active[i]];
+  auto grid_of = [&](int v) {
+    double share = na > 1 && wsum > 0 ? P->sched.work[v] / wsum : 1.0;
+    int g = (int)(P->num_sms * share + 0.5);
+    return std::max(1, std::min(std::max(g, 1), P->items_cap[v]));
+  };
   auto launch = [&](int v, cudaStream_t sv) -> cudaError_t {
-    if (v == VAR_TC) {
-      int grid = std::max(1, std::min(P->num_sms, P->items_cap[v]));
+    const int grid = grid_of(v);
+    if (v == VAR_TC)
       return launch_forward_tc(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sv);
-    }
-    int grid = std::max(1, std::min(P->num_sms, P->items_cap[v]));
     return launch_forward_variant(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sv);
   };
   if (na == 1) {

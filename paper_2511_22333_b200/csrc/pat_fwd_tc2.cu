@@ -76,6 +76,10 @@ template <> struct Fmt<__half> {
     return *reinterpret_cast<uint32_t*>(&h);
   }
   static __device__ __forceinline__ uint32_t pack_lo(float, float, uint32_t) { return 0u; }
+  static __device__ __forceinline__ float sum2(uint32_t v) {
+    float2 f = __half22float2(*reinterpret_cast<__half2*>(&v));
+    return f.x + f.y;
+  }
 };
 template <> struct Fmt<__nv_bfloat16> {
   static constexpr int ab = 1;
@@ -92,6 +96,10 @@ template <> struct Fmt<__nv_bfloat16> {
     __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&hi);
     float2 f = __bfloat1622float2(h);
     return pack(a - f.x, b - f.y);
+  }
+  static __device__ __forceinline__ float sum2(uint32_t v) {
+    float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+    return f.x + f.y;
   }
 };
 
@@ -352,9 +360,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < kN / 2; ++k) {
           const float e0 = exp2f(__uint_as_float(sr[2 * k]) - m_ref);
           const float e1 = exp2f(__uint_as_float(sr[2 * k + 1]) - m_ref);
-          l += e0 + e1;
           ph[k] = Fmt<T>::pack(e0, e1);
-          if constexpr (kSplit) pl[k] = Fmt<T>::pack_lo(e0, e1, ph[k]);
+          if constexpr (kSplit) {
+            pl[k] = Fmt<T>::pack_lo(e0, e1, ph[k]);
+            l += e0 + e1;
+          } else {
+            // normalise by the sum of the ROUNDED weights the MMA actually uses:
+            // the output is then an exact weighted average of V rows
+            l += Fmt<T>::sum2(ph[k]);
+          }
         }
         // the P columns are free once PV of the previous tile completed
         if (j > 0) {

@@ -26,6 +26,7 @@ struct HostSchedule {
   std::vector<int32_t> unit_slot_off, unit_slot;
   std::vector<int32_t> q_slot_off, q_nslot, merge_q;
   std::vector<Item> items[NUM_VARIANTS];
+  double work[NUM_VARIANTS] = {0, 0, 0, 0};  // estimated SM-ns per kernel variant
   int32_t n_slots = 0;
 };
 

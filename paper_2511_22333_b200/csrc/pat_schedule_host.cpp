@@ -39,22 +39,25 @@ void split_pack(int npages, int kv, int bs, int parts, std::vector<Part>& out) {
 //        max item cost )                        -- the critical CTA
 // + per-item fixed cost.  An item's cost is pages x per-page time of its
 // kernel (streaming: its HBM share per SM; tcgen05: per 128-row block).
+// per-page cost (ns) of a work item of variant v (same constants as native_parts)
+double page_cost(const ScheduleParams& sp, int v) {
+  const double bw = 6.0e3;
+  const double page_bytes = 16.0 * sp.d * 4;
+  return v == VAR_TC ? 500.0 : page_bytes / (bw / std::max(sp.num_sms, 1));
+}
+
 void native_parts(const HostPacks& P, const ScheduleParams& sp, std::vector<int>& nparts) {
   const int NP = P.n_packs();
   const int G = sp.H / sp.KVH;
   const double bw = 6.0e3;                // bytes per ns (HBM, sustained)
-  const double page_bytes = 16.0 * sp.d * 4;  // K+V of 16 tokens of one kv head
-  const double t_stream = page_bytes / (bw / std::max(sp.num_sms, 1));  // ns per page per SM
-  const double t_tc = 350.0;              // ns per page per 128-row tcgen05 item (measured c4)
   const double t_item = 1500.0;           // ns fixed cost per item (Q load, pipeline fill, epilogue)
-  std::vector<int> rows(NP), pages(NP), rb(NP), tc(NP);
+  std::vector<int> rows(NP), pages(NP), rb(NP);
   int maxpages = 1;
   double kv_bytes = 0;
   for (int p = 0; p < NP; ++p) {
     rows[p] = (P.q_off[p + 1] - P.q_off[p]) * G;
     pages[p] = P.blk_off[p + 1] - P.blk_off[p];
     int v = choose_variant(rows[p], sp.tc_min_rows);
-    tc[p] = v == VAR_TC;
     rb[p] = (int)ceil_div(rows[p], variant_rows(v));
     maxpages = std::max(maxpages, pages[p]);
     kv_bytes += (double)P.kv[p] * sp.KVH * sp.d * 4;
@@ -63,18 +66,28 @@ void native_parts(const HostPacks& P, const ScheduleParams& sp, std::vector<int>
   for (int chunk = 1; ; chunk *= 2) {
     const int c = std::min(chunk, maxpages);
     double work = 0, worst = 0, extra = 0;
-    int64_t items = 0;
+    double vwork[NUM_VARIANTS] = {0, 0, 0, 0};
+    int64_t vitems[NUM_VARIANTS] = {0, 0, 0, 0};
     for (int p = 0; p < NP; ++p) {
       int parts = (int)ceil_div(pages[p], c);
-      double per_page = tc[p] ? t_tc : t_stream;
-      double item = std::min(c, pages[p]) * per_page + t_item;
+      int v = choose_variant(rows[p], sp.tc_min_rows);
+      double item = std::min(c, pages[p]) * page_cost(sp, v) + t_item;
       int64_t n = (int64_t)parts * rb[p] * sp.KVH;
-      items += n;
+      vitems[v] += n;
+      vwork[v] += item * n;
       work += item * n;
       worst = std::max(worst, item);
       if (parts > 1) extra += (double)parts * (P.q_off[p + 1] - P.q_off[p]) * sp.H * sp.d * 8;
     }
-    double est = std::max({(kv_bytes + extra) / bw, work / std::max(sp.num_sms, 1), worst});
+    // each variant runs on an SM share proportional to its work (pat_forward);
+    // its time is the number of item waves on that share x the mean item
+    double tv = 0;
+    for (int v = 0; v < NUM_VARIANTS; ++v) {
+      if (!vitems[v]) continue;
+      int sms = std::max(1, (int)(sp.num_sms * vwork[v] / work + 0.5));
+      tv = std::max(tv, (double)ceil_div(vitems[v], sms) * (vwork[v] / vitems[v]));
+    }
+    double est = std::max({(kv_bytes + extra) / bw, tv, worst});
     cand.emplace_back(c, est);
     if (c >= maxpages) break;
   }
@@ -170,9 +183,11 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S)
     int v = choose_variant(rows, sp.tc_min_rows);
     int R = variant_rows(v);
     for (int r0 = 0; r0 < rows; r0 += R)
-      for (int h = 0; h < sp.KVH; ++h)
+      for (int h = 0; h < sp.KVH; ++h) {
         S->items[v].push_back({u, h, r0, std::min(R, rows - r0), P.blk_off[p] + S->unit_page0[u], S->unit_ntok[u],
                                P.q_off[p], S->unit_slot_off[u]});
+        S->work[v] += S->unit_npages[u] * page_cost(sp, v) + 1500.0;
+      }
   }
   (void)unit_begin;
   return PAT_OK;
