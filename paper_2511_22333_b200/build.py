@@ -17,6 +17,7 @@ SOURCES = [
     "pat_fwd_mma.cu",
     "pat_fwd_tc2.cu",
     "pat_packer_host.cpp",
+    "pat_packer_dev.cu",
     "pat_schedule_host.cpp",
 ]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

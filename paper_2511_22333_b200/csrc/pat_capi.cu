@@ -33,6 +33,9 @@ cudaError_t launch_forward_tc(const CUtensorMap& tmk, const CUtensorMap& tmv, co
                               int dtype, int d, const void* q, void* out, float* po, float* pl, float scale_log2,
                               cudaStream_t st);
 int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t num_blocks, int bs, int kvh, int d, int dtype);
+int device_pack(const int32_t* d_bt, int64_t stride, const int32_t* d_seq, int B, int maxb, int bs, cudaStream_t st,
+                HostPacks* out, std::vector<int32_t>* h_nblk, std::vector<int32_t>* h_valid,
+                std::vector<int32_t>* h_rows);
 
 }  // namespace pat
 
@@ -454,11 +457,29 @@ void pat_plan_destroy(pat_plan* P) {
 int pat_plan_create_device(int32_t B, const int32_t* block_tables, int64_t bt_stride, const int32_t* seq_lens,
                            int32_t max_blocks, int32_t block_size, const pat_plan_options* opt, void* stream,
                            pat_plan** out) {
-  (void)B; (void)block_tables; (void)bt_stride; (void)seq_lens; (void)max_blocks; (void)block_size; (void)opt;
-  (void)stream;
-  if (out) *out = nullptr;
-  set_error("device packer not built yet");
-  return PAT_ERR_INTERNAL;
+  if (!out) return PAT_ERR_INVALID_SPEC;
+  *out = nullptr;
+  int st = check_opts(opt);
+  if (st) return st;
+  if (B < 0 || max_blocks < 1 || bt_stride < max_blocks || block_size <= 0 || (B > 0 && (!block_tables || !seq_lens))) {
+    set_error("bad block-table arguments");
+    return PAT_ERR_SHAPE_MISMATCH;
+  }
+  pat_plan* P = new pat_plan();
+  init_plan(P, B, block_size, opt);
+  std::vector<int32_t> nblk, valid, rows;
+  st = device_pack(block_tables, bt_stride, seq_lens, B, max_blocks, block_size, (cudaStream_t)stream, &P->packs,
+                   &nblk, &valid, &rows);
+  if (!st) {
+    RowsView R{rows.data(), nullptr, bt_stride, nblk.data(), valid.data(), B, block_size};
+    st = finish_plan(P, R, opt->flags);
+  }
+  if (st) {
+    pat_plan_destroy(P);
+    return st;
+  }
+  *out = P;
+  return PAT_OK;
 }
 
 }  // extern "C"

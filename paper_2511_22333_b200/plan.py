@@ -55,6 +55,26 @@ class PatPlan:
         return cls(h, num_heads, num_kv_heads, head_dim)
 
     @classmethod
+    def from_device_table(cls, block_tables, seq_lens, block_size=16, num_heads=32, num_kv_heads=8, head_dim=128,
+                          split="native", num_sms=0, tc_min_rows=0, stream=None) -> "PatPlan":
+        """GPU packer (``pat_plan_create_device``) on device block tables [B, max_blocks]
+        and seq lens [B] (int32 CUDA tensors, vLLM layout)."""
+        import torch
+
+        if block_tables.dtype != torch.int32 or seq_lens.dtype != torch.int32 or not block_tables.is_cuda:
+            raise InvalidSpec("block_tables / seq_lens must be int32 CUDA tensors")
+        bt = block_tables.contiguous()
+        sl = seq_lens.contiguous()
+        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, False, num_sms, tc_min_rows)
+        s = stream if stream is not None else torch.cuda.current_stream(bt.device)
+        h = C.c_void_p()
+        st = N.lib().pat_plan_create_device(bt.shape[0], C.c_void_p(bt.data_ptr()), bt.shape[1],
+                                            C.c_void_p(sl.data_ptr()), bt.shape[1], block_size, C.byref(opt),
+                                            C.c_void_p(s.cuda_stream), C.byref(h))
+        N.check(st, "pat_plan_create_device")
+        return cls(h, num_heads, num_kv_heads, head_dim)
+
+    @classmethod
     def from_units(cls, table, units, num_heads=32, num_kv_heads=8, head_dim=128, split="none", host_only=False,
                    num_sms=0, tc_min_rows=0) -> "PatPlan":
         """Explicit partition: ``units`` = [(query_ids, block_ids, kv_len)] in fold order."""

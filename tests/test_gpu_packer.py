@@ -1,0 +1,73 @@
+"""GPU packer (pat_plan_create_device) vs the reference plans: bit-exact on the
+2,855-tree family, the random/edge corpus and c1..c5, from vLLM-layout device
+block tables; invalid tables raise InvalidSpec."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2511_22333_b200 as P
+from paper_2511_22333_b200 import configs
+from paper_2511_22333_b200.plan import PatPlan
+
+from golden_io import as_packs, config_cases, family_cases, random_cases
+
+pytestmark = pytest.mark.gpu
+
+
+def _device_packs(rows, valid, bs, extra_cols=0):
+    t = P.BlockTable([list(r) for r in rows], list(valid), bs)
+    bt, sl = t.padded((max(len(r) for r in rows) if rows else 1) + extra_cols)
+    plan = PatPlan.from_device_table(torch.from_numpy(bt).cuda(), torch.from_numpy(sl).cuda(), block_size=bs,
+                                     num_heads=8, num_kv_heads=2, head_dim=128, split="none")
+    try:
+        return plan.pack_tuples()
+    finally:
+        plan.close()
+
+
+def test_tree_family_device_bit_exact():
+    for c in family_cases():
+        assert _device_packs(c["rows"], c["valid"], c["bs"]) == as_packs(c["packs"]), c["name"]
+
+
+def test_random_edge_device_bit_exact():
+    doc = random_cases()
+    for i, c in enumerate(doc["cases"]):
+        if not c["rows"]:
+            continue
+        got = _device_packs(c["rows"], c["valid"], c["bs"], extra_cols=i % 3)
+        assert got == as_packs(c["packs"]), c["name"]
+
+
+def test_configs_device_bit_exact():
+    cc = config_cases()
+    for name in configs.ALL:
+        w = configs.workload(name)
+        assert _device_packs(w.rows, w.valid_last, w.block_size) == as_packs(cc[name]["packs"]), name
+
+
+def test_device_invalid_tables():
+    bt = torch.tensor([[0, 1, 0]], dtype=torch.int32, device="cuda")
+    with pytest.raises(P.InvalidSpec):
+        PatPlan.from_device_table(bt, torch.tensor([40], dtype=torch.int32, device="cuda"), num_heads=8,
+                                  num_kv_heads=2)
+    with pytest.raises(P.InvalidSpec):
+        PatPlan.from_device_table(bt, torch.tensor([0], dtype=torch.int32, device="cuda"), num_heads=8,
+                                  num_kv_heads=2)
+
+
+def test_device_plan_forward_matches_host_plan():
+    w = configs.workload("c2")
+    t = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    bt, sl = t.padded()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    nb = w.num_pool_blocks()
+    kc = torch.randn(nb, 16, 8, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    vc = torch.randn(nb, 16, 8, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    q = torch.randn(w.batch, 32, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    pd = PatPlan.from_device_table(torch.from_numpy(bt).cuda(), torch.from_numpy(sl).cuda())
+    ph = PatPlan.from_table(t)
+    assert pd.pack_tuples() == ph.pack_tuples()
+    assert torch.equal(P.pat_attention(pd, q, kc, vc), P.pat_attention(ph, q, kc, vc))
+    assert np.isfinite(1.0)
