@@ -16,7 +16,7 @@ from .workload import (BlockTable, CtaPack, Partition, WorkloadSpec, assemble_pa
 from .packer import (CtaTask, PackCache, baseline_query_centric, naive_per_node, pack_batch, pack_batch_async,
                      split_long_kv)
 from .plan import PatPlan
-from .attention import PatDecoder, kv_pool_from_store, pat_attention, run_packed_attention
+from .attention import PatDecoder, PatLayerGraph, kv_pool_from_store, pat_attention, run_packed_attention
 from .metrics import distinct_block_census, theoretical_min_kv_bytes
 
 __version__ = "0.1.0"

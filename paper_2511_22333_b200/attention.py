@@ -101,6 +101,34 @@ class PatDecoder:
         return pat_attention(plan, q, k_cache, v_cache, out=out, workspace=self.workspace(plan), scale=scale)
 
 
+class PatLayerGraph:
+    """One decode-attention layer captured as a CUDA graph (the multi-stream
+    fork/join inside ``pat_forward`` is captured too); ``replay()`` re-runs it on
+    the same buffers with a single launch.  The plan and tensors must stay alive
+    and in place (lazy update: rebuild the graph when the plan changes)."""
+
+    def __init__(self, plan: PatPlan, q, k_cache, v_cache, out=None, workspace=None, scale=None):
+        self.plan, self.q, self.k_cache, self.v_cache = plan, q, k_cache, v_cache
+        self.out = out if out is not None else torch.empty_like(q)
+        need = max(plan.workspace_bytes(), 256)
+        self.ws = workspace if workspace is not None else torch.empty(need, dtype=torch.uint8, device=q.device)
+        self.scale = scale
+        # warm-up outside capture: kernel attributes, tensor maps, side streams
+        pat_attention(plan, q, k_cache, v_cache, out=self.out, workspace=self.ws, scale=scale)
+        torch.cuda.synchronize(q.device)
+        self.graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(q.device)
+        s.wait_stream(torch.cuda.current_stream(q.device))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(self.graph, stream=s):
+                pat_attention(plan, q, k_cache, v_cache, out=self.out, workspace=self.ws, scale=scale, stream=s)
+        torch.cuda.current_stream(q.device).wait_stream(s)
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
+
+
 def kv_pool_from_store(kv_store: dict, block_size: int, dtype=torch.float16, device="cuda"):
     """Paged caches [max_id + 1, page, KVH, d] from the reference ``{id: (K, V)}`` store."""
     ids = sorted(kv_store)
@@ -144,4 +172,5 @@ def run_packed_attention(table: BlockTable, partition_or_tasks: Union[Partition,
         plan.close()
 
 
-__all__ = ["run_packed_attention", "pat_attention", "PatDecoder", "kv_pool_from_store", "CoverageGap"]
+__all__ = ["run_packed_attention", "pat_attention", "PatDecoder", "PatLayerGraph", "kv_pool_from_store",
+           "CoverageGap"]

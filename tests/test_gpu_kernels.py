@@ -105,3 +105,25 @@ def test_variant_configs_vs_oracle(name, tc):
         bad = err > 2e-3 + 1e-2 * np.abs(ref)
         heads = sorted(set(np.nonzero(bad)[0].tolist()))
         assert not bad.any(), f"q{qi}: {bad.sum()} bad, heads {heads[:16]}, max err {err.max():.3e}"
+
+
+def test_cuda_graph_replay_matches_eager():
+    w = configs.workload("c2")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    nb = w.num_pool_blocks()
+    kc = torch.randn(nb, 16, 8, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    vc = torch.randn(nb, 16, 8, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    q = torch.randn(w.batch, 32, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    plan = PatPlan.from_table(table)
+    eager = P.pat_attention(plan, q, kc, vc).clone()
+    graph = P.PatLayerGraph(plan, q, kc, vc)
+    graph.out.zero_()
+    got = graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(got, eager)
+    q.mul_(0.5)  # in-place input update is seen by the next replay
+    eager2 = P.pat_attention(plan, q, kc, vc)
+    got2 = graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(got2, eager2)

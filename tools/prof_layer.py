@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--tc", type=int, default=0)
     ap.add_argument("--split", default="native")
     ap.add_argument("--dtype", default="bfloat16")
+    ap.add_argument("--graph", action="store_true")
     args = ap.parse_args()
     w = configs.workload(args.config)
     dt = getattr(torch, args.dtype)
@@ -39,11 +40,15 @@ def main():
     out = torch.empty_like(q)
     ws = torch.empty(max(plan.workspace_bytes(), 256), dtype=torch.uint8, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    g = P.PatLayerGraph(plan, q, kc, vc, out=out, workspace=ws) if args.graph else None
     for i in range(args.warmup + args.iters):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        P.pat_attention(plan, q, kc, vc, out=out, workspace=ws)
+        if g is not None:
+            g.replay()
+        else:
+            P.pat_attention(plan, q, kc, vc, out=out, workspace=ws)
         b.record()
         torch.cuda.synchronize()
         if i >= args.warmup:
