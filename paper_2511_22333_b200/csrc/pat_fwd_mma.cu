@@ -525,7 +525,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   }
 }
 
-// One warp per (query, head): fold the query's slots with online softmax.
+// One warp per (query, head): fold the query's slots with online softmax
+// (_merge_batch_into, attention.py:187-199).  Latency-bound, so: lanes fetch
+// up to 32 slot LSEs at once, weights are shuffled, and the weighted O rows are
+// independent loads issued 4 at a time.
 template <int D, typename T>
 __global__ void __launch_bounds__(256) merge_kernel(DevPlan plan, const float* __restrict__ part_o,
                                                     const float* __restrict__ part_lse, T* __restrict__ out) {
@@ -536,28 +539,49 @@ __global__ void __launch_bounds__(256) merge_kernel(DevPlan plan, const float* _
   const int nw = (gridDim.x * blockDim.x) >> 5;
   constexpr int PER = D / 32;
   for (int w = gw; w < nq * H; w += nw) {
-    const int q = plan.merge_q[w / H], head = w % H;
-    const int base = plan.q_slot_off[q], n = plan.q_nslot[q];
-    float M = -INFINITY;
-    for (int i = lane; i < n; i += 32) M = fmaxf(M, part_lse[(int64_t)(base + i) * H + head]);
-#pragma unroll
-    for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    const int q = __ldg(plan.merge_q + w / H), head = w % H;
+    const int base = __ldg(plan.q_slot_off + q), n = __ldg(plan.q_nslot + q);
     float acc[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) acc[e] = 0.f;
-    float L = 0.f;
-    for (int i = 0; i < n; ++i) {
-      const int64_t s = (int64_t)(base + i) * H + head;
-      const float f = exp2f(part_lse[s] - M);
-      L += f;
-      const float* src = part_o + s * D + lane * PER;
+    float M = -INFINITY, L = 0.f;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int cn = min(32, n - c0);
+      const float lse = lane < cn ? __ldg(part_lse + (int64_t)(base + c0 + lane) * H + head) : -INFINITY;
+      float cm = lse;
 #pragma unroll
-      for (int e = 0; e < PER; e += 4) {
-        float4 v = *reinterpret_cast<const float4*>(src + e);
-        acc[e] += f * v.x;
-        acc[e + 1] += f * v.y;
-        acc[e + 2] += f * v.z;
-        acc[e + 3] += f * v.w;
+      for (int off = 16; off; off >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, off));
+      const float Mn = fmaxf(M, cm);
+      const float a = exp2f(M - Mn);  // rescale what was accumulated so far
+#pragma unroll
+      for (int e = 0; e < PER; ++e) acc[e] *= a;
+      L *= a;
+      M = Mn;
+      const float f = lane < cn ? exp2f(lse - M) : 0.f;
+      float fs = f;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) fs += __shfl_xor_sync(0xffffffffu, fs, off);
+      L += fs;
+      for (int i = 0; i < cn; i += 4) {
+        float v[4][PER];
+        float fi[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          fi[u] = __shfl_sync(0xffffffffu, f, min(i + u, 31));
+          const float* src = part_o + ((int64_t)(base + c0 + min(i + u, cn - 1)) * H + head) * D + lane * PER;
+          if constexpr (PER == 4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+            v[u][0] = x.x, v[u][1] = x.y, v[u][2] = x.z, v[u][3] = x.w;
+          } else {
+            const float2 x = __ldg(reinterpret_cast<const float2*>(src));
+            v[u][0] = x.x, v[u][1] = x.y;
+          }
+          if (i + u >= cn) fi[u] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int e = 0; e < PER; ++e) acc[e] += fi[u] * v[u][e];
       }
     }
     const float inv = 1.f / L;
