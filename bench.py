@@ -34,6 +34,19 @@ METRIC = "decode attn latency µs/layer + achieved HBM GB/s (unique KV) vs roofl
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def load_traffic(config):
+    """Per-layer DRAM bytes (read + write) of the layer's kernels from a committed
+    ncu capture (profiles/round*_traffic_<config>.json), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", f"round*_traffic_{config}.json")))
+    if not files:
+        return None
+    with open(files[-1]) as fh:
+        d = json.load(fh)
+    return {"bytes": int(d["layer_dram_bytes"]), "source": os.path.relpath(files[-1], REPO)}
+
+
 def load_peaks():
     p = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -220,8 +233,12 @@ def measure_config(name, rank, world, steps, warmup, dev, flush, split="native",
     ws = torch.empty(max(plan.workspace_bytes(), 256), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    # production decode replays a captured graph of the layer (forward kernels on
+    # their streams + merge); the e2e leg below goes through the eager API
+    graph = P.PatLayerGraph(plan, q, kc, vc, out=out, workspace=ws)
+
     def layer():
-        P.pat_attention(plan, q, kc, vc, out=out, workspace=ws)
+        graph.replay()
 
     for _ in range(warmup):
         flush.zero_()
@@ -382,6 +399,7 @@ def main():
         except Exception as exc:  # keep the GPU line even if the CPU leg fails
             cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
+    traffic = load_traffic(args.config) if world == 1 else None
     if rank == 0:
         gbs = tot_bytes / (t_ms * 1e-3) / 1e9
         info = main_res["info"]
@@ -397,8 +415,10 @@ def main():
                        "unique_kv_bytes": int(tot_bytes), "packs": info.n_packs, "units": info.n_units,
                        "work_items": info.n_items, "merge_queries": info.n_merge_q},
             "roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": None,
-                         "kernel": "one layer: pat forward kernels (all variants, multi-stream) + merge",
+                         "frac": round(gbs / peaks["hbm_gbs"], 4),
+                         "traffic": traffic["bytes"] if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else None,
+                         "kernel": "one decode-attention layer (CUDA graph: forward kernels on their SM shares + merge); traffic = sum of its kernels (ncu)",
                          "peak_source": peaks["source"]},
             "e2e": {"value": round(tot_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": main_res["e2e"]["h2d"], "d2h_bytes_per_step": main_res["e2e"]["d2h"],
