@@ -71,8 +71,9 @@ typedef struct pat_plan_options {
   int32_t split_mode;   /* pat_split_mode */
   int32_t num_sms;      /* 0 = query the current device */
   int32_t flags;        /* pat_plan_flags */
-  int32_t tc_min_rows;  /* packs with >= this many rows (queries x G) use the tcgen05 kernel;
-                           0 = default (64), < 0 = never */
+  int32_t tc_min_rows;  /* packs with >= this many rows (queries x G) use the tcgen05 kernel,
+                           the others the mma.sync streaming kernel; 0 = default (1: every
+                           pack on the tcgen05 kernel), < 0 = never */
 } pat_plan_options;
 
 typedef struct pat_plan_info {

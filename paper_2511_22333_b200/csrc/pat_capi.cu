@@ -102,7 +102,7 @@ void init_plan(pat_plan* P, int B, int bs, const pat_plan_options* opt) {
   P->d = opt->head_dim;
   P->split_mode = opt->split_mode;
   P->num_sms = opt->num_sms;
-  P->tc_min_rows = opt->tc_min_rows == 0 ? 64 : (opt->tc_min_rows < 0 ? 0 : opt->tc_min_rows);
+  P->tc_min_rows = opt->tc_min_rows == 0 ? 1 : (opt->tc_min_rows < 0 ? 0 : opt->tc_min_rows);
   if (P->d != 64 && P->d != 128) P->tc_min_rows = 0;
   if (P->num_sms <= 0) {
     int dev = 0, n = 0;
@@ -146,6 +146,8 @@ int upload(pat_plan* P) {
   size_t o_mq = b.addv(s.merge_q), o_qso = b.addv(s.q_slot_off), o_qn = b.addv(s.q_nslot);
   int32_t nm = (int32_t)s.merge_q.size();
   size_t o_nm = b.add(&nm, sizeof(nm));
+  const int32_t zeros[16] = {};
+  size_t o_sched = b.add(zeros, sizeof(zeros));
   CUDA_TRY(cudaGetDevice(&P->device));
   CUDA_TRY(cudaMalloc(&P->dmem, b.bytes.size()));
   CUDA_TRY(cudaMemcpy(P->dmem, b.bytes.data(), b.bytes.size(), cudaMemcpyHostToDevice));
@@ -166,6 +168,7 @@ int upload(pat_plan* P) {
   D.q_slot_off = (const int32_t*)(base + o_qso);
   D.q_nslot = (const int32_t*)(base + o_qn);
   D.n_merge = (const int32_t*)(base + o_nm);
+  D.sched = (int32_t*)(base + o_sched);
   D.H = P->H;
   D.KVH = P->KVH;
   D.d = P->d;

@@ -41,4 +41,31 @@ struct RowsView {
 
 PAT_HD int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Debug builds (-DPAT_TC_TRACE, tools/layer_trace.py): per-CTA [start, end]
+// globaltimer spans of a kernel, one array per translation unit.
+#ifdef PAT_TC_TRACE
+constexpr int kSpanCtas = 1024;
+__device__ __forceinline__ unsigned long long pat_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PAT_SPAN_BEGIN(arr, k)                                                \
+  do {                                                                        \
+    if (threadIdx.x == 0 && blockIdx.x < pat::kSpanCtas) arr[k][blockIdx.x][0] = pat::pat_gtime(); \
+  } while (0)
+#define PAT_SPAN_END(arr, k)                                                  \
+  do {                                                                        \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < pat::kSpanCtas)               \
+      atomicMax(&arr[k][blockIdx.x][1], pat::pat_gtime());                    \
+  } while (0)
+#else
+#define PAT_SPAN_BEGIN(arr, k) \
+  do {                         \
+  } while (0)
+#define PAT_SPAN_END(arr, k) \
+  do {                       \
+  } while (0)
+#endif
+
 }  // namespace pat

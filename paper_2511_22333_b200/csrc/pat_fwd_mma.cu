@@ -104,6 +104,10 @@ __device__ __forceinline__ uint32_t swz_q(int r, int ch) {
   return (uint32_t)(line * 128 + (((ch & 7) ^ (r & 7)) << 4));
 }
 
+#ifdef PAT_TC_TRACE
+__device__ unsigned long long g_span_mma[2][kSpanCtas][2];  // [stream, merge][cta][start, end]
+#endif
+
 template <int WM, int D>
 struct StreamSmem {
   static constexpr int KB = D / 64;
@@ -207,6 +211,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  PAT_SPAN_BEGIN(g_span_mma, 0);
 
   if (warp == 4) {
     // ------------------------------------------------------------ producer
@@ -523,6 +528,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     meta_qid = next_qid;
     meta_slot = next_slot;
   }
+  PAT_SPAN_END(g_span_mma, 0);
 }
 
 // One warp per (query, head): fold the query's slots with online softmax
@@ -532,6 +538,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 template <int D, typename T>
 __global__ void __launch_bounds__(256) merge_kernel(DevPlan plan, const float* __restrict__ part_o,
                                                     const float* __restrict__ part_lse, T* __restrict__ out) {
+  PAT_SPAN_BEGIN(g_span_mma, 1);
   const int H = plan.H;
   const int nq = *plan.n_merge;
   const int lane = threadIdx.x & 31;
@@ -592,7 +599,17 @@ __global__ void __launch_bounds__(256) merge_kernel(DevPlan plan, const float* _
       *reinterpret_cast<uint32_t*>(dst + e) = pk;
     }
   }
+  PAT_SPAN_END(g_span_mma, 1);
 }
+
+#ifdef PAT_TC_TRACE
+extern "C" int pat_debug_spans_mma(unsigned long long* host) {
+  int e = (int)cudaMemcpyFromSymbol(host, g_span_mma, sizeof(g_span_mma));
+  static unsigned long long zero[2][kSpanCtas][2];
+  cudaMemcpyToSymbol(g_span_mma, zero, sizeof(zero));
+  return e;
+}
+#endif
 
 // ------------------------------------------------------------------------------------------
 // launchers

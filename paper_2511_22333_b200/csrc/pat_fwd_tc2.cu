@@ -32,10 +32,25 @@
 namespace pat {
 namespace tc2 {
 
-constexpr int kThreads = 384;
+#ifdef PAT_TC_TRACE
+// Debug timeline (tools/tc_trace.py): CTA 0 records clock64 per (role, event, step).
+// roles: 0 producer, 1 MMA issuer, 2 softmax tile A (warp 4 lane 0), 3 softmax tile B.
+constexpr int kTraceSteps = 256;
+__device__ long long g_tc_trace[4][8][kTraceSteps];
+__device__ unsigned long long g_span_tc[1][kSpanCtas][2];
+#define TC_TRACE(role, ev, step)                                        \
+  do {                                                                  \
+    if (blockIdx.x == 0 && (step) < kTraceSteps) g_tc_trace[role][ev][step] = clock64(); \
+  } while (0)
+#else
+#define TC_TRACE(role, ev, step) \
+  do {                           \
+  } while (0)
+#endif
+constexpr int kThreads = 576;  // producer, MMA issuer (+TMEM alloc), 16 softmax warps
 constexpr int kM = 128;       // rows per tile
 constexpr int kN = 64;        // tokens per KV tile
-constexpr int kStages = 5;
+constexpr int kStages = 4;
 constexpr uint32_t kTmemCols = 512;
 #ifndef PAT_TC_RESCALE_THRESHOLD
 #define PAT_TC_RESCALE_THRESHOLD 8.0f
@@ -50,7 +65,8 @@ struct Layout {
   static constexpr int kOffQ = 0;                    // Q_A, Q_B
   static constexpr int kOffKV = 2 * kQBytes;
   static constexpr int kOffBar = kOffKV + kStages * 2 * kTileBytes;
-  static constexpr int kBytes = kOffBar + 512;
+  static constexpr int kOffRed = kOffBar + 512;         // row-max / row-sum exchange
+  static constexpr int kBytes = kOffRed + 2 * 2 * 2 * kM * 4;
   static constexpr int kAlloc = kBytes + 1024;
 };
 
@@ -64,8 +80,11 @@ enum Bar : int {
   O_EMPTY = O_DONE + 2,         // [tile]
   Q_FULL = O_EMPTY + 2,         // [tile]
   Q_EMPTY = Q_FULL + 2,         // [tile]
-  NUM_BARS = Q_EMPTY + 2
+  ITEM_FULL = Q_EMPTY + 2,      // [slot] work-item index published by the producer
+  ITEM_EMPTY = ITEM_FULL + 2,   // [slot] read by the MMA warp and the 16 softmax warps
+  NUM_BARS = ITEM_EMPTY + 2
 };
+constexpr int kItemReaders = 17;
 
 template <typename T> struct Fmt;
 template <> struct Fmt<__half> {
@@ -76,9 +95,8 @@ template <> struct Fmt<__half> {
     return *reinterpret_cast<uint32_t*>(&h);
   }
   static __device__ __forceinline__ uint32_t pack_lo(float, float, uint32_t) { return 0u; }
-  static __device__ __forceinline__ float sum2(uint32_t v) {
-    float2 f = __half22float2(*reinterpret_cast<__half2*>(&v));
-    return f.x + f.y;
+  static __device__ __forceinline__ float2 unpack(uint32_t v) {
+    return __half22float2(*reinterpret_cast<__half2*>(&v));
   }
 };
 template <> struct Fmt<__nv_bfloat16> {
@@ -97,15 +115,28 @@ template <> struct Fmt<__nv_bfloat16> {
     float2 f = __bfloat1622float2(h);
     return pack(a - f.x, b - f.y);
   }
-  static __device__ __forceinline__ float sum2(uint32_t v) {
-    float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
-    return f.x + f.y;
+  static __device__ __forceinline__ float2 unpack(uint32_t v) {
+    return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
   }
 };
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ Item load_item(const Item* p) {
@@ -128,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sKV = sb + L::kOffKV;
   const uint32_t bars = sb + L::kOffBar;
   uint32_t* tmem_slot = (uint32_t*)(smem + L::kOffBar + NUM_BARS * 8);
+  volatile int32_t* item_ring = (volatile int32_t*)(smem + L::kOffBar + NUM_BARS * 8 + 16);
   auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
   auto sQ = [&](int x) { return sb + L::kOffQ + (uint32_t)(x * L::kQBytes); };
   auto sK = [&](int s) { return sKV + (uint32_t)(s * 2 * L::kTileBytes); };
@@ -145,37 +177,67 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(S_FULL + i), 1);
-      mbar_init(bar(S_EMPTY + i), 4);
-      mbar_init(bar(P_FULL + i), 4);
+      mbar_init(bar(S_EMPTY + i), 8);
+      mbar_init(bar(P_FULL + i), 8);
     }
     for (int x = 0; x < 2; ++x) {
       mbar_init(bar(O_DONE + x), 1);
-      mbar_init(bar(O_EMPTY + x), 4);
-      mbar_init(bar(Q_FULL + x), 4);
+      mbar_init(bar(O_EMPTY + x), 8);
+      mbar_init(bar(Q_FULL + x), 8);
       mbar_init(bar(Q_EMPTY + x), 1);
+      mbar_init(bar(ITEM_FULL + x), 1);
+      mbar_init(bar(ITEM_EMPTY + x), kItemReaders);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(smem_u32(tmem_slot));
+  if (warp == 1) tmem_alloc<kTmemCols>(smem_u32(tmem_slot));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  PAT_SPAN_BEGIN(g_span_tc, 0);
   // TMEM columns: S[x] at 128x, P[x] at 128x + 64 (hi: +0..31, lo: +32..63),
   // O[x] at 256 + 128x.  P has its own columns: a PV MMA reading P from TMEM
   // must never share columns with a later QK MMA's accumulator (measured WAR
   // hazard when P lived inside the double-buffered S region).
+  // Dynamic work distribution: the producer claims items (in the scheduler's
+  // longest-first order) from a global counter one item ahead and publishes
+  // the index through a 2-slot shared ring; the MMA warp and the softmax
+  // warps follow the same sequence.  -1 ends the loop.
+  auto next_item = [&](uint32_t n) -> int {
+    const uint32_t slot = n & 1;
+    mbar_wait(bar(ITEM_FULL + slot), (n >> 1) & 1);
+    const int it = item_ring[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + slot));
+    return it;
+  };
   auto tS = [&](int x) { return tmem + (uint32_t)(128 * x); };
   auto tP = [&](int x) { return tmem + (uint32_t)(128 * x + 64); };
   auto tO = [&](int x) { return tmem + 256u + (uint32_t)(128 * x); };
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (one thread)
-    if (lane == 0) {
-      tma_prefetch(&tmk);
-      tma_prefetch(&tmv);
+    // ------------------------------------------------------------ TMA producer
+    // Whole warp: lane i fetches the block id of page group i of the stage,
+    // broadcast by shuffle (warp-uniform operands), one elected lane issues.
+    {
+      if (elect_one()) {
+        tma_prefetch(&tmk);
+        tma_prefetch(&tmv);
+      }
       uint32_t g = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t slot = n & 1;
+        mbar_wait(bar(ITEM_EMPTY + slot), ((n >> 1) & 1) ^ 1);
+        int it = 0;
+        if (lane == 0) {
+          it = atomicAdd(plan.sched, 1);
+          if (it >= n_items) it = -1;
+          item_ring[slot] = it;
+          mbar_arrive(bar(ITEM_FULL + slot));
+        }
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it < 0) break;
         const Item item = load_item(items + it);
         const int h = item.kvh, ntok = item.ntok;
         const int32_t* blist = plan.pack_blk + item.blk;
@@ -184,57 +246,85 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = g % kStages;
           const int rem = ntok - j * kN;
           const int ngrp = rem >= kN ? kN / 16 : (rem + 15) / 16;
-          mbar_wait(bar(KV_EMPTY + s), ((g / kStages) & 1) ^ 1);
-          mbar_expect_tx(bar(KV_FULL + s), (uint32_t)(ngrp * L::KB * 2048 * 2));
-          for (int gr = 0; gr < ngrp; ++gr) {
-            const int tok = j * kN + gr * 16;
+          int my_blk = 0, my_off = 0;
+          if (lane < ngrp) {
+            const int tok = j * kN + lane * 16;
             const int pg = bs == 16 ? (tok >> 4) : tok / bs;
-            const int blk = __ldg(blist + pg);
-            const int off = bs == 16 ? 0 : tok - pg * bs;
+            my_blk = __ldg(blist + pg);
+            my_off = bs == 16 ? 0 : tok - pg * bs;
+          }
+          mbar_wait(bar(KV_EMPTY + s), ((g / kStages) & 1) ^ 1);
+          TC_TRACE(0, 0, g);
+          if (elect_one()) mbar_expect_tx(bar(KV_FULL + s), (uint32_t)(ngrp * L::KB * 2048 * 2));
+          __syncwarp();
+          for (int gr = 0; gr < ngrp; ++gr) {
+            const int blk = __shfl_sync(0xffffffffu, my_blk, gr);
+            const int off = __shfl_sync(0xffffffffu, my_off, gr);
+            if (elect_one()) {
 #pragma unroll
-            for (int kb = 0; kb < L::KB; ++kb) {
-              tma_load_4d(sK(s) + kb * (kN * 128) + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
-              tma_load_4d(sV(s) + kb * (kN * 128) + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
+              for (int kb = 0; kb < L::KB; ++kb) {
+                tma_load_4d(sK(s) + kb * (kN * 128) + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
+                tma_load_4d(sV(s) + kb * (kN * 128) + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
+              }
             }
+            __syncwarp();
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (one thread)
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    // The whole warp runs the loop so descriptors and TMEM addresses stay
+    // warp-uniform (uniform datapath, no per-MMA waterfall); one elected lane
+    // issues each tcgen05.mma / commit (CUTLASS's elect_one_sync pattern).
+    {
       constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
       constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
       uint32_t g = 0;           // KV tiles consumed
       uint32_t c[2] = {0, 0};   // KV tiles processed per query tile (S/P buffer index)
       uint32_t ni[2] = {0, 0};  // items processed per query tile
+      auto commit = [&](int b) {
+        if (elect_one()) umma_commit(bar(b));
+        __syncwarp();
+      };
       auto issue_qk = [&](int x, int s, uint32_t ci) {
         // S[x] is single-buffered: wait until the softmax has read tile ci-1
         mbar_wait(bar(S_EMPTY + x), (ci & 1) ^ 1);
+        if (x == 0) TC_TRACE(1, 3, g);
         tc_fence_after();
+        const uint64_t a0 = umma_desc_sw128(sQ(x), 16, 1024), b0 = umma_desc_sw128(sK(s), 16, 1024);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const int kb = k >> 2, kk = k & 3;
-          uint64_t a = umma_desc_sw128(sQ(x) + kb * (kM * 128) + kk * 32, 16, 1024);
-          uint64_t bd = umma_desc_sw128(sK(s) + kb * (kN * 128) + kk * 32, 16, 1024);
-          umma_f16_ss(tS(x), a, bd, idesc_qk, k > 0 ? 1u : 0u);
+          for (int k = 0; k < D / 16; ++k) {
+            const int kb = k >> 2, kk = k & 3;
+            // descriptor start address is in 16-byte units (bits 0-13)
+            umma_f16_ss(tS(x), a0 + (uint64_t)((kb * (kM * 128) + kk * 32) >> 4),
+                        b0 + (uint64_t)((kb * (kN * 128) + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
+          }
         }
+        __syncwarp();
       };
       auto issue_pv = [&](int x, int s, uint32_t ci, bool first) {
         if (first) mbar_wait(bar(O_EMPTY + x), (ni[x] & 1) ^ 1);
         mbar_wait(bar(P_FULL + x), ci & 1);
+        if (x == 0) TC_TRACE(1, 4, g);
         tc_fence_after();
-
+        const uint64_t v0 = umma_desc_sw128(sV(s), kN * 128, 1024);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < kN / 16; ++k) {
-          uint64_t bd = umma_desc_sw128(sV(s) + k * 16 * 128, kN * 128, 1024);
-          // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
-          umma_f16_ts(tO(x), tP(x) + k * 8, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
-          if constexpr (kSplit) umma_f16_ts(tO(x), tP(x) + 32 + k * 8, bd, idesc_pv, 1u);
+          for (int k = 0; k < kN / 16; ++k) {
+            const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
+            // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
+            umma_f16_ts(tO(x), tP(x) + k * 8, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
+            if constexpr (kSplit) umma_f16_ts(tO(x), tP(x) + 32 + k * 8, bd, idesc_pv, 1u);
+          }
+          umma_commit(bar(O_DONE + x));
         }
-        umma_commit(bar(O_DONE + x));
+        __syncwarp();
       };
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      for (uint32_t n = 0;; ++n) {
+        const int it = next_item(n);
+        if (it < 0) break;
         const Item item = load_item(items + it);
         const bool liveB = item.nrows > kM;
         const int ntiles = (item.ntok + kN - 1) / kN;
@@ -245,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < ntiles; ++j, ++g) {
           const int s = g % kStages;
           mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
+          TC_TRACE(1, 0, g);
           tc_fence_after();
           // Both tiles' S MMAs are issued before either S_FULL is signalled:
           // a softmax must not read/write its S region while the OTHER tile's
@@ -252,22 +343,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           // regions are 128 or 256 TMEM columns apart; tools/tc_debug.py).
           issue_qk(0, s, c[0] + j);
           if (liveB) issue_qk(1, s, c[1] + j);
-          umma_commit(bar(S_FULL + 0));
-          if (liveB) umma_commit(bar(S_FULL + 1));
+          commit(S_FULL + 0);
+          if (liveB) commit(S_FULL + 1);
           if (j == ntiles - 1) {
-            umma_commit(bar(Q_EMPTY + 0));
-            if (liveB) umma_commit(bar(Q_EMPTY + 1));
+            commit(Q_EMPTY + 0);
+            if (liveB) commit(Q_EMPTY + 1);
           }
+          TC_TRACE(1, 1, g);
           if (j > 0) {
             issue_pv(0, sprev, c[0] + j - 1, j == 1);
+            TC_TRACE(1, 2, g);
             if (liveB) issue_pv(1, sprev, c[1] + j - 1, j == 1);
-            umma_commit(bar(KV_EMPTY + sprev));
+            commit(KV_EMPTY + sprev);
           }
           sprev = s;
         }
         issue_pv(0, sprev, c[0] + ntiles - 1, ntiles == 1);
         if (liveB) issue_pv(1, sprev, c[1] + ntiles - 1, ntiles == 1);
-        umma_commit(bar(KV_EMPTY + sprev));
+        commit(KV_EMPTY + sprev);
         c[0] += ntiles;
         ++ni[0];
         if (liveB) {
@@ -276,14 +369,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  } else {
     // ------------------------------------------------------------ softmax / epilogue
-    const int x = (warp - 4) >> 2;       // query tile
-    const int t = tid - 128 - x * 128;   // row in the tile == TMEM lane
-    const int wg = (warp - 4) & 3;       // lane quarter
-    const uint32_t lane_base = (uint32_t)(wg * 32) << 16;
-    uint32_t c = 0, ni = 0, g = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    // 16 warps (2-17): tile x = sw >> 3, column half h = (sw >> 2) & 1, lane
+    // quarter wq = warp % 4 (the TMEM lanes the warp may access).  The two
+    // halves of a row (same lanes, same SMSP) exchange their partial row max
+    // through shared memory each KV tile, so both keep the same running max.
+    const int sw = warp - 2;
+    const int x = sw >> 3, h = (sw >> 2) & 1, wq = warp & 3;
+    const int t = wq * 32 + lane;                 // row in the tile == TMEM lane
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const uint32_t pair_bar = 1 + x * 4 + wq;     // named barrier of the two half-warps
+    float* red = reinterpret_cast<float*>(smem + L::kOffRed);  // [2 parity][2 tile][2 half][128]
+    auto red_at = [&](uint32_t par, int hh) { return red + ((par * 2 + x) * 2 + hh) * kM + t; };
+    uint32_t c = 0, ni = 0, g = 0, xc = 0;  // xc: exchange-buffer uses
+    for (uint32_t n = 0;; ++n) {
+      const int it = next_item(n);
+      if (it < 0) break;
       const Item item = load_item(items + it);
       const int ntok = item.ntok;
       const int ntiles = (ntok + kN - 1) / kN;
@@ -291,21 +393,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         g += ntiles;
         continue;  // tile B idle for this item
       }
-      const int h = item.kvh;
+      const int hd = item.kvh;
       const int r = x * kM + t;  // row within the item
       const bool live = r < item.nrows;
       const int row = item.row0 + r;
       const int qi = live ? row / G : 0;
       const int qid = live ? __ldg(plan.pack_q + item.qoff + qi) : 0;
-      const int head = h * G + (live ? row % G : 0);
+      const int head = hd * G + (live ? row % G : 0);
       const int slot = live ? __ldg(plan.unit_slot + item.slot_off + qi) : -1;
 
-      // Q row -> smem (after the previous item's last QK of this tile)
+      // Q row half -> smem (after the previous item's last QK of this tile)
       mbar_wait(bar(Q_EMPTY + x), (ni & 1) ^ 1);
       {
         const uint4* src = reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + head) * D);
+        constexpr int kCh = D / 16;  // 16-byte chunks per half row
 #pragma unroll
-        for (int ch = 0; ch < D / 8; ++ch) {
+        for (int i = 0; i < kCh; ++i) {
+          const int ch = h * kCh + i;
           uint4 v = live ? __ldg(src + ch) : make_uint4(0, 0, 0, 0);
           st_shared_v4(sQ(x) + (ch >> 3) * (kM * 128) + t * 128 + (((ch & 7) ^ (t & 7)) << 4), v);
         }
@@ -314,76 +418,93 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(Q_FULL + x));
 
-      float m_ref = -INFINITY, l = 0.f;
+      float m_ref = -INFINITY;  // running max, log2 units
+      float2 l2 = make_float2(0.f, 0.f);
       for (int j = 0; j < ntiles; ++j, ++c, ++g) {
         mbar_wait(bar(S_FULL + x), c & 1);
+        if (t == 0 && h == 0) TC_TRACE(2 + x, 0, g);
         tc_fence_after();
-        uint32_t sr[kN];
-        tmem_ld32(tS(x) + lane_base, sr);
-        tmem_ld32(tS(x) + lane_base + 32, sr + 32);
+        uint32_t sr[32];
+        tmem_ld32(tS(x) + lane_base + 32 * h, sr);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(S_EMPTY + x));
-        tmem_wait_ld();
 
-        const int valid = ntok - j * kN;
-        float mx = -INFINITY;
+        const int valid = ntok - j * kN - 32 * h;  // valid columns of this half
+        if (valid < 32) {
 #pragma unroll
-        for (int k = 0; k < kN; ++k) {
-          float v = k < valid ? __uint_as_float(sr[k]) * scale_log2 : -INFINITY;
-          sr[k] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
+          for (int k = 0; k < 32; ++k)
+            if (k >= valid) sr[k] = __float_as_uint(-INFINITY);
         }
+        float pm[11];
+#pragma unroll
+        for (int k = 0; k < 10; ++k)
+          pm[k] = fmax3(__uint_as_float(sr[3 * k]), __uint_as_float(sr[3 * k + 1]), __uint_as_float(sr[3 * k + 2]));
+        pm[10] = fmaxf(__uint_as_float(sr[30]), __uint_as_float(sr[31]));
+        float pmx = fmax3(fmax3(pm[0], pm[1], pm[2]), fmax3(pm[3], pm[4], pm[5]),
+                          fmax3(fmax3(pm[6], pm[7], pm[8]), pm[9], pm[10]));
+        *red_at(xc & 1, h) = pmx;
+        named_bar_sync(pair_bar, 64);
+        const float mx = fmaxf(pmx, *red_at(xc & 1, h ^ 1)) * scale_log2;
+        ++xc;
         const bool need = mx > m_ref + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
           const float m_new = need ? mx : m_ref;
-          const float alpha = exp2f(m_ref - m_new);
+          const float alpha = ex2_approx(m_ref - m_new);
           if (j > 0) {
             mbar_wait(bar(O_DONE + x), (c - 1) & 1);
             tc_fence_after();
 #pragma unroll
             for (int q = 0; q < D / 32; ++q) {
-              uint32_t o[32];
-              tmem_ld32(tO(x) + lane_base + q * 32, o);
-              tmem_wait_ld();
+              uint32_t o[16];
+              const uint32_t ta = tO(x) + lane_base + (uint32_t)(h * (D / 2) + q * 16);
+              tmem_ld16(ta, o);
 #pragma unroll
-              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-              tmem_st32(tO(x) + lane_base + q * 32, o);
+              for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              tmem_st16_wait(ta, o);
             }
           }
-          l *= alpha;
+          l2.x *= alpha;
+          l2.y *= alpha;
           m_ref = m_new;
         }
-        // P = exp2(s - m_ref), packed 16-bit pairs, stored over S (hi: cols 0-31, lo: 32-63)
-        uint32_t ph[kN / 2], pl[kN / 2];
+        // P = exp2(s * scale - m_ref), packed 16-bit pairs (hi: 16 cols, lo: 16 cols)
+        const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_ref, -m_ref);
+        uint32_t ph[16], pl[16];
 #pragma unroll
-        for (int k = 0; k < kN / 2; ++k) {
-          const float e0 = exp2f(__uint_as_float(sr[2 * k]) - m_ref);
-          const float e1 = exp2f(__uint_as_float(sr[2 * k + 1]) - m_ref);
-          ph[k] = Fmt<T>::pack(e0, e1);
+        for (int k = 0; k < 16; ++k) {
+          float2 a = __ffma2_rn(make_float2(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sc2, nm2);
+          a.x = ex2_approx(a.x);
+          a.y = ex2_approx(a.y);
+          ph[k] = Fmt<T>::pack(a.x, a.y);
           if constexpr (kSplit) {
-            pl[k] = Fmt<T>::pack_lo(e0, e1, ph[k]);
-            l += e0 + e1;
+            const float2 hf = make_float2(__uint_as_float(ph[k] << 16), __uint_as_float(ph[k] & 0xffff0000u));
+            const float2 lo = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
+            pl[k] = Fmt<T>::pack(lo.x, lo.y);
+            l2 = __fadd2_rn(l2, a);
           } else {
             // normalise by the sum of the ROUNDED weights the MMA actually uses:
             // the output is then an exact weighted average of V rows
-            l += Fmt<T>::sum2(ph[k]);
+            l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
           }
         }
+        if (t == 0 && h == 0) TC_TRACE(2 + x, 1, g);
         // the P columns are free once PV of the previous tile completed
         if (j > 0) {
           mbar_wait(bar(O_DONE + x), (c - 1) & 1);
           tc_fence_after();
         }
-        tmem_st32(tP(x) + lane_base, ph);
-        if constexpr (kSplit) tmem_st32(tP(x) + lane_base + 32, pl);
-        if (valid < kN) {
+        if (t == 0 && h == 0) TC_TRACE(2 + x, 2, g);
+        tmem_st16(tP(x) + lane_base + 16 * h, ph);
+        if constexpr (kSplit) tmem_st16(tP(x) + lane_base + 32 + 16 * h, pl);
+        if (j * kN + kN > ntok) {
           // tail tile: zero V rows past the span (both tiles may do it: same zeros)
+          const int vt = ntok - j * kN;
           const int s = g % kStages;
           mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
-          const int nz = (kN - valid) * L::KB * 8;
-          for (int q = t; q < nz; q += 128) {
-            const int rr = valid + q / (L::KB * 8);
+          const int nz = (kN - vt) * L::KB * 8;
+          for (int q = h * kM + t; q < nz; q += 2 * kM) {
+            const int rr = vt + q / (L::KB * 8);
             const int kb = (q / 8) % L::KB, ch = q % 8;
             st_shared_v4(sV(s) + kb * (kN * 128) + rr * 128 + (ch << 4), make_uint4(0, 0, 0, 0));
           }
@@ -393,48 +514,64 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(P_FULL + x));
+        if (t == 0 && h == 0) TC_TRACE(2 + x, 3, g);
       }
 
-      // epilogue: O / l
+      // epilogue: O / l; the halves exchange their partial l
+      float lh = l2.x + l2.y;
+      *red_at(xc & 1, h) = lh;
+      named_bar_sync(pair_bar, 64);
+      const float l = lh + *red_at(xc & 1, h ^ 1);
+      ++xc;
       mbar_wait(bar(O_DONE + x), (c - 1) & 1);
       tc_fence_after();
       const float inv = 1.f / l;
 #pragma unroll
       for (int q = 0; q < D / 32; ++q) {
-        uint32_t o[32];
-        tmem_ld32(tO(x) + lane_base + q * 32, o);
-        tmem_wait_ld();
+        uint32_t o[16];
+        const int col = h * (D / 2) + q * 16;
+        tmem_ld16(tO(x) + lane_base + (uint32_t)col, o);
         if (live) {
           if (slot < 0) {
-            uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)qid * H + head) * D + q * 32);
+            uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)qid * H + head) * D + col);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < 2; ++k) {
               const float* f = reinterpret_cast<const float*>(o + k * 8);
               dst[k] = make_uint4(Fmt<T>::pack(f[0] * inv, f[1] * inv), Fmt<T>::pack(f[2] * inv, f[3] * inv),
                                   Fmt<T>::pack(f[4] * inv, f[5] * inv), Fmt<T>::pack(f[6] * inv, f[7] * inv));
             }
           } else {
-            float4* dst = reinterpret_cast<float4*>(part_o + ((int64_t)slot * H + head) * D + q * 32);
+            float4* dst = reinterpret_cast<float4*>(part_o + ((int64_t)slot * H + head) * D + col);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < 4; ++k) {
               const float* f = reinterpret_cast<const float*>(o + k * 4);
               dst[k] = make_float4(f[0] * inv, f[1] * inv, f[2] * inv, f[3] * inv);
             }
           }
         }
       }
-      if (live && slot >= 0) part_lse[(int64_t)slot * H + head] = m_ref + log2f(l);
+      if (live && slot >= 0 && h == 0) part_lse[(int64_t)slot * H + head] = m_ref + log2f(l);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(O_EMPTY + x));
       ++ni;
     }
   }
+  PAT_SPAN_END(g_span_tc, 0);
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
+  }
+  if (tid == 0) {
+    // the last CTA out re-arms the item counter for the next launch
+    __threadfence();
+    if (atomicAdd(plan.sched + 1, 1) == (int)gridDim.x - 1) {
+      plan.sched[0] = 0;
+      plan.sched[1] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -487,6 +624,18 @@ static cudaError_t launch_tc2_t(const CUtensorMap& tmk, const CUtensorMap& tmv, 
                                                                scale_log2);
   return cudaGetLastError();
 }
+
+#ifdef PAT_TC_TRACE
+extern "C" int pat_debug_tc_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, tc2::g_tc_trace, sizeof(tc2::g_tc_trace));
+}
+extern "C" int pat_debug_spans_tc(unsigned long long* host) {
+  int e = (int)cudaMemcpyFromSymbol(host, tc2::g_span_tc, sizeof(tc2::g_span_tc));
+  static unsigned long long zero[1][kSpanCtas][2];
+  cudaMemcpyToSymbol(tc2::g_span_tc, zero, sizeof(zero));
+  return e;
+}
+#endif
 
 cudaError_t launch_forward_tc(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var, int grid,
                               int dtype, int d, const void* q, void* out, float* po, float* pl, float scale_log2,

@@ -55,6 +55,8 @@ struct DevPlan {
   const int32_t* q_slot_off;    // [B] first slot of the query
   const int32_t* q_nslot;       // [B] slots of the query (0 or >= 2)
   const int32_t* n_merge;       // [1]
+  int32_t* sched;               // [2] dynamic item counter, finished CTAs (tcgen05 kernel;
+                                //     zero between launches: the last CTA resets them)
   int32_t H, KVH, d, G, bs;
 };
 

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <cmath>
 #include <numeric>
+#include <cstdio>
+#include <cstdlib>
 
 #include "pat_plan_host.h"
 
@@ -32,71 +34,89 @@ void split_pack(int npages, int kv, int bs, int parts, std::vector<Part>& out) {
 }
 
 
+// Estimated time (ns) of one work item of variant v with `rows` rows over
+// `ntok` tokens, measured on B200 (tools/tc_trace.py): the tcgen05 kernel runs
+// a 64-token KV tile in ~0.75 us for <= 128 rows and ~1.26 us for 256 rows
+// (softmax / MMA-issue bound, close to one SM's HBM share of 32 KB per 0.7 us
+// when all SMs stream); the mma.sync streaming kernel is HBM-paced.  Fixed
+// cost: Q load, pipeline fill and the epilogue.
+double item_ns(const ScheduleParams& sp, int v, int rows, int ntok) {
+  const double steps = (double)ceil_div(ntok, 64);
+  const double dscale = sp.d / 128.0;
+  if (v == VAR_TC) return 1500.0 + steps * (rows > 128 ? 1260.0 : 750.0) * (0.5 + 0.5 * dscale);
+  const double bw = 6.0e3;  // bytes per ns (HBM, sustained)
+  return 1500.0 + steps * 64.0 * sp.d * 4 / (bw / std::max(sp.num_sms, 1));
+}
+
 // Native KV split for B200.  Picks one chunk size (pages) for all packs by
 // minimising a makespan estimate over candidate chunks:
 //   max( bytes(chunk) / HBM_BW,                 -- KV + extra fp32 partials
-//        work(chunk) / num_SMs,                 -- all items spread over SMs
+//        sum(item cost) / SMs per variant,      -- dynamic (tcgen05) or wave-
+//                                                  quantised (static) scheduling
 //        max item cost )                        -- the critical CTA
-// + per-item fixed cost.  An item's cost is pages x per-page time of its
-// kernel (streaming: its HBM share per SM; tcgen05: per 128-row block).
-// per-page cost (ns) of a work item of variant v (same constants as native_parts)
-double page_cost(const ScheduleParams& sp, int v) {
-  const double bw = 6.0e3;
-  const double page_bytes = 16.0 * sp.d * 4;
-  return v == VAR_TC ? 500.0 : page_bytes / (bw / std::max(sp.num_sms, 1));
-}
-
 void native_parts(const HostPacks& P, const ScheduleParams& sp, std::vector<int>& nparts) {
   const int NP = P.n_packs();
   const int G = sp.H / sp.KVH;
-  const double bw = 6.0e3;                // bytes per ns (HBM, sustained)
-  const double t_item = 1500.0;           // ns fixed cost per item (Q load, pipeline fill, epilogue)
-  std::vector<int> rows(NP), pages(NP), rb(NP);
+  const double bw = 6.0e3;  // bytes per ns (HBM, sustained)
+  std::vector<int> rows(NP), pages(NP);
   int maxpages = 1;
   double kv_bytes = 0;
   for (int p = 0; p < NP; ++p) {
     rows[p] = (P.q_off[p + 1] - P.q_off[p]) * G;
     pages[p] = P.blk_off[p + 1] - P.blk_off[p];
-    int v = choose_variant(rows[p], sp.tc_min_rows);
-    rb[p] = (int)ceil_div(rows[p], variant_rows(v));
     maxpages = std::max(maxpages, pages[p]);
     kv_bytes += (double)P.kv[p] * sp.KVH * sp.d * 4;
   }
   std::vector<std::pair<int, double>> cand;
-  for (int chunk = 1; ; chunk *= 2) {
+  std::vector<double> worsts;
+  for (int chunk = 1;; chunk *= 2) {
     const int c = std::min(chunk, maxpages);
     double work = 0, worst = 0, extra = 0;
     double vwork[NUM_VARIANTS] = {0, 0, 0, 0};
     int64_t vitems[NUM_VARIANTS] = {0, 0, 0, 0};
     for (int p = 0; p < NP; ++p) {
-      int parts = (int)ceil_div(pages[p], c);
-      int v = choose_variant(rows[p], sp.tc_min_rows);
-      double item = std::min(c, pages[p]) * page_cost(sp, v) + t_item;
-      int64_t n = (int64_t)parts * rb[p] * sp.KVH;
-      vitems[v] += n;
-      vwork[v] += item * n;
-      work += item * n;
-      worst = std::max(worst, item);
+      const int parts = (int)ceil_div(pages[p], c);
+      const int v = choose_variant(rows[p], sp.tc_min_rows);
+      const int R = variant_rows(v);
+      const int ntok = std::min(c, pages[p]) * sp.bs;
+      for (int r0 = 0; r0 < rows[p]; r0 += R) {
+        const double item = item_ns(sp, v, std::min(R, rows[p] - r0), ntok);
+        const int64_t n = (int64_t)parts * sp.KVH;
+        vitems[v] += n;
+        vwork[v] += item * n;
+        work += item * n;
+        worst = std::max(worst, item);
+      }
       if (parts > 1) extra += (double)parts * (P.q_off[p + 1] - P.q_off[p]) * sp.H * sp.d * 8;
     }
-    // each variant runs on an SM share proportional to its work (pat_forward);
-    // its time is the number of item waves on that share x the mean item
+    // each variant runs on an SM share proportional to its work (pat_forward)
     double tv = 0;
     for (int v = 0; v < NUM_VARIANTS; ++v) {
       if (!vitems[v]) continue;
-      int sms = std::max(1, (int)(sp.num_sms * vwork[v] / work + 0.5));
-      tv = std::max(tv, (double)ceil_div(vitems[v], sms) * (vwork[v] / vitems[v]));
+      const int sms = std::max(1, (int)(sp.num_sms * vwork[v] / work + 0.5));
+      const double mean = vwork[v] / vitems[v];
+      if (v == VAR_TC)  // dynamic longest-first: average load plus half a mean item of tail
+        tv = std::max(tv, vwork[v] / sms + 0.5 * mean);
+      else
+        tv = std::max(tv, (double)ceil_div(vitems[v], sms) * mean);
     }
-    double est = std::max({(kv_bytes + extra) / bw, tv, worst});
+    const double est = std::max({(kv_bytes + extra) / bw, tv, worst});
     cand.emplace_back(c, est);
+    worsts.push_back(worst);
+    if (getenv("PAT_DEBUG_SPLIT")) fprintf(stderr, "chunk %d bytes %.1f tv %.1f worst %.1f est %.1f\n", c, (kv_bytes + extra) / bw / 1e3, tv / 1e3, worst / 1e3, est / 1e3);
     if (c >= maxpages) break;
   }
   double best = 1e300;
   for (auto& ce : cand) best = std::min(best, ce.second);
-  int best_chunk = maxpages;  // the largest chunk within 2% of the best estimate: fewest splits
-  for (auto& ce : cand)
-    if (ce.second <= best * 1.02) best_chunk = std::max(best_chunk == maxpages ? 0 : best_chunk, ce.first);
-  if (best_chunk <= 0) best_chunk = maxpages;
+  // the largest chunk within 3% of the best estimate (fewest splits) whose
+  // longest item stays under half the makespan (robust to cost-model error)
+  int best_chunk = 0;
+  for (size_t i = 0; i < cand.size(); ++i)
+    if (cand[i].second <= best * 1.03 && worsts[i] <= 0.5 * cand[i].second)
+      best_chunk = std::max(best_chunk, cand[i].first);
+  if (best_chunk <= 0)
+    for (auto& ce : cand)
+      if (ce.second == best) best_chunk = ce.first;
   for (int p = 0; p < NP; ++p) nparts[p] = (int)ceil_div(pages[p], best_chunk);
 }
 
@@ -172,22 +192,32 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S)
     S->unit_slot_off.push_back((int32_t)S->unit_slot.size());
   }
 
-  // 4. work items, longest first within each kernel variant
-  std::vector<int> order(NU);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int a, int b) { return S->unit_npages[a] > S->unit_npages[b]; });
-  for (int u : order) {
+  // 4. work items (unit x row block x kv head), longest (estimated) first
+  // within each kernel variant: the tcgen05 kernel hands them out dynamically,
+  // so this is longest-processing-time-first list scheduling.
+  struct Cand {
+    Item it;
+    double ns;
+    int v;
+  };
+  std::vector<Cand> cands;
+  for (int u = 0; u < NU; ++u) {
     int p = S->unit_pack[u];
     int rows = (P.q_off[p + 1] - P.q_off[p]) * G;
     int v = choose_variant(rows, sp.tc_min_rows);
     int R = variant_rows(v);
-    for (int r0 = 0; r0 < rows; r0 += R)
-      for (int h = 0; h < sp.KVH; ++h) {
-        S->items[v].push_back({u, h, r0, std::min(R, rows - r0), P.blk_off[p] + S->unit_page0[u], S->unit_ntok[u],
-                               P.q_off[p], S->unit_slot_off[u]});
-        S->work[v] += S->unit_npages[u] * page_cost(sp, v) + 1500.0;
-      }
+    for (int r0 = 0; r0 < rows; r0 += R) {
+      const double ns = item_ns(sp, v, std::min(R, rows - r0), S->unit_ntok[u]);
+      for (int h = 0; h < sp.KVH; ++h)
+        cands.push_back({{u, h, r0, std::min(R, rows - r0), P.blk_off[p] + S->unit_page0[u], S->unit_ntok[u],
+                          P.q_off[p], S->unit_slot_off[u]},
+                         ns, v});
+    }
+  }
+  std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.ns > b.ns; });
+  for (const Cand& c : cands) {
+    S->items[c.v].push_back(c.it);
+    S->work[c.v] += c.ns;
   }
   (void)unit_begin;
   return PAT_OK;

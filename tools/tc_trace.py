@@ -1,0 +1,100 @@
+"""Timeline of the tcgen05 forward kernel (CTA 0) on one wide pack.
+
+    python tools/tc_trace.py --build            # here: compile tools/libpat_trace.so (-DPAT_TC_TRACE)
+    python tools/tc_trace.py [--nq 32 --G 8 --kvh 8 --ntok 8192]   # on the GPU box
+
+Prints the kernel time (CUDA events) and, per KV step of CTA 0, the clock64
+deltas between the producer / MMA issuer / softmax events (a debugging tool,
+not a bench number)."""
+
+import argparse
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TRACE_LIB = os.path.join(REPO, "tools", "libpat_trace.so")
+sys.path.insert(0, REPO)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--build", action="store_true")
+    ap.add_argument("--defines", default="")
+    ap.add_argument("--nq", type=int, default=32)
+    ap.add_argument("--G", type=int, default=8)
+    ap.add_argument("--kvh", type=int, default=8)
+    ap.add_argument("--ntok", type=int, default=8192)
+    ap.add_argument("--steps", type=int, default=24)
+    ap.add_argument("--lib", default=TRACE_LIB)
+    ap.add_argument("--dtype", default="bfloat16")
+    args = ap.parse_args()
+    if args.build:
+        from paper_2511_22333_b200 import build as B
+        defs = ["PAT_TC_TRACE"] + [d for d in args.defines.split(",") if d]
+        print(B.build(force=True, out=args.lib, defines=defs))
+        return
+    os.environ["PAT_LIB"] = args.lib
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2511_22333_b200 as P
+    from paper_2511_22333_b200 import _native as N
+
+    bs, nq, G, KVH, ntok = 16, args.nq, args.G, args.kvh, args.ntok
+    H = G * KVH
+    nblk = ntok // bs
+    table = P.BlockTable([list(range(nblk)) for _ in range(nq)], [bs] * nq, bs)
+    plan = P.PatPlan.from_table(table, H, KVH, 128, split="none", tc_min_rows=1)
+    inf = plan.info()
+    dt = getattr(torch, args.dtype)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    kc = torch.randn(nblk, bs, KVH, 128, device="cuda", dtype=dt, generator=g)
+    vc = torch.randn(nblk, bs, KVH, 128, device="cuda", dtype=dt, generator=g)
+    q = torch.randn(nq, H, 128, device="cuda", dtype=dt, generator=g)
+    out = torch.empty_like(q)
+    ws = torch.empty(max(plan.workspace_bytes(), 256), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    times = []
+    for i in range(6):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        P.pat_attention(plan, q, kc, vc, out=out, workspace=ws)
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b) * 1e3)
+    us = min(times[2:])
+    kv_bytes = ntok * KVH * 128 * 4
+    flops = 4.0 * nq * H * ntok * 128
+    print(f"rows/item {nq * G} items {inf.n_items} kv {ntok}x{KVH}: layer {us:.1f} us  "
+          f"{kv_bytes / us / 1e3:.0f} GB/s  {flops / us / 1e6:.1f} TFLOP/s")
+    tr = np.zeros((4, 8, 256), dtype=np.int64)
+    lib = N.lib()
+    lib.pat_debug_tc_trace.argtypes = [C.c_void_p]
+    assert lib.pat_debug_tc_trace(tr.ctypes.data) == 0
+    t0 = tr[0, 0, 0]
+    names = {(0, 0): "prod_kvempty", (1, 0): "mma_kvfull", (1, 3): "qkA_start", (1, 1): "mma_qk_issued",
+             (1, 4): "pvA_start(j-1)", (1, 2): "mma_pv_issued",
+             (2, 0): "smA_sfull", (2, 1): "smA_exp_done", (2, 2): "smA_odone", (2, 3): "smA_pfull",
+             (3, 0): "smB_sfull", (3, 1): "smB_exp_done", (3, 2): "smB_odone", (3, 3): "smB_pfull"}
+    hdr = " step " + " ".join(f"{v:>14s}" for v in names.values())
+    print(hdr)
+    n = min(args.steps, ntok // 64)
+    for s in range(n):
+        row = []
+        for (r, e) in names:
+            v = tr[r, e, s]
+            row.append(f"{(v - t0) if v else -1:>14d}")
+        print(f"{s:5d} " + " ".join(row))
+    # steady-state per-step cycles from the MMA issuer's KV_FULL timestamps
+    m = tr[1, 0, :n]
+    m = m[m > 0]
+    if len(m) > 4:
+        d = np.diff(m[2:])
+        print(f"steady-state cycles/step (mma kvfull): median {np.median(d):.0f} mean {d.mean():.0f}")
+
+
+if __name__ == "__main__":
+    main()
