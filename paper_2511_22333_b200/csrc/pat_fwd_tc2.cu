@@ -66,7 +66,8 @@ struct Layout {
   static constexpr int kOffKV = 2 * kQBytes;
   static constexpr int kOffBar = kOffKV + kStages * 2 * kTileBytes;
   static constexpr int kOffRed = kOffBar + 512;         // row-max / row-sum exchange
-  static constexpr int kBytes = kOffRed + 2 * 2 * 2 * kM * 4;
+  static constexpr int kOffRing = kOffRed + 2 * 2 * 2 * kM * 4;  // 2 x ItemSlot
+  static constexpr int kBytes = kOffRing + 2 * 2112;
   static constexpr int kAlloc = kBytes + 1024;
 };
 
@@ -85,6 +86,17 @@ enum Bar : int {
   NUM_BARS = ITEM_EMPTY + 2
 };
 constexpr int kItemReaders = 17;
+
+// One slot of the work-item ring: the item and, per row, the query id and
+// partial slot resolved by the producer warp (so consumers never chase the
+// pack_q / unit_slot indirections at an item boundary).
+struct ItemSlot {
+  int32_t idx;
+  int32_t pad[7];
+  Item item;
+  int2 meta[2 * 128];  // (qid, slot) per row
+};
+static_assert(sizeof(ItemSlot) == 2112, "ItemSlot layout");
 
 template <typename T> struct Fmt;
 template <> struct Fmt<__half> {
@@ -135,6 +147,12 @@ __device__ __forceinline__ float ex2_approx(float v) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
   return r;
 }
+// 16-byte global -> shared async copy; src_size 0 zero-fills the destination
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -159,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sKV = sb + L::kOffKV;
   const uint32_t bars = sb + L::kOffBar;
   uint32_t* tmem_slot = (uint32_t*)(smem + L::kOffBar + NUM_BARS * 8);
-  volatile int32_t* item_ring = (volatile int32_t*)(smem + L::kOffBar + NUM_BARS * 8 + 16);
+  ItemSlot* ring = reinterpret_cast<ItemSlot*>(smem + L::kOffRing);
   auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
   auto sQ = [&](int x) { return sb + L::kOffQ + (uint32_t)(x * L::kQBytes); };
   auto sK = [&](int s) { return sKV + (uint32_t)(s * 2 * L::kTileBytes); };
@@ -185,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(O_EMPTY + x), 8);
       mbar_init(bar(Q_FULL + x), 8);
       mbar_init(bar(Q_EMPTY + x), 1);
-      mbar_init(bar(ITEM_FULL + x), 1);
+      mbar_init(bar(ITEM_FULL + x), 32);
       mbar_init(bar(ITEM_EMPTY + x), kItemReaders);
     }
     fence_mbar_init();
@@ -204,10 +222,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   // longest-first order) from a global counter one item ahead and publishes
   // the index through a 2-slot shared ring; the MMA warp and the softmax
   // warps follow the same sequence.  -1 ends the loop.
-  auto next_item = [&](uint32_t n) -> int {
+  // Returns the item index (-1 = done), the item and, for row `r` (< 0: none),
+  // its (qid, slot) metadata.
+  auto next_item = [&](uint32_t n, Item& itm, int r, int2& meta) -> int {
     const uint32_t slot = n & 1;
     mbar_wait(bar(ITEM_FULL + slot), (n >> 1) & 1);
-    const int it = item_ring[slot];
+    const ItemSlot* rs = ring + slot;  // plain loads: ordered by the mbarrier wait (asm memory clobber)
+    const int it = rs->idx;
+    if (it >= 0) {
+      itm = rs->item;
+      if (r >= 0 && r < itm.nrows) meta = rs->meta[r];
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + slot));
     return it;
@@ -233,12 +258,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           it = atomicAdd(plan.sched, 1);
           if (it >= n_items) it = -1;
-          item_ring[slot] = it;
-          mbar_arrive(bar(ITEM_FULL + slot));
         }
         it = __shfl_sync(0xffffffffu, it, 0);
+        Item item{};
+        if (it >= 0) {
+          item = load_item(items + it);
+          for (int r = lane; r < item.nrows; r += 32) {
+            const int qi = (item.row0 + r) / G;
+            ring[slot].meta[r] = make_int2(__ldg(plan.pack_q + item.qoff + qi), __ldg(plan.unit_slot + item.slot_off + qi));
+          }
+          if (lane == 0) ring[slot].item = item;
+        }
+        if (lane == 0) ring[slot].idx = it;
+        __syncwarp();
+        mbar_arrive(bar(ITEM_FULL + slot));
         if (it < 0) break;
-        const Item item = load_item(items + it);
         const int h = item.kvh, ntok = item.ntok;
         const int32_t* blist = plan.pack_blk + item.blk;
         const int ntiles = (ntok + kN - 1) / kN;
@@ -323,13 +357,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       };
       for (uint32_t n = 0;; ++n) {
-        const int it = next_item(n);
-        if (it < 0) break;
-        const Item item = load_item(items + it);
+        Item item;
+        int2 unused;
+        if (next_item(n, item, -1, unused) < 0) break;
         const bool liveB = item.nrows > kM;
         const int ntiles = (item.ntok + kN - 1) / kN;
         mbar_wait(bar(Q_FULL + 0), ni[0] & 1);
         if (liveB) mbar_wait(bar(Q_FULL + 1), ni[1] & 1);
+        TC_TRACE(1, 5, g);
         tc_fence_after();
         int sprev = 0;
         for (int j = 0; j < ntiles; ++j, ++g) {
@@ -383,40 +418,69 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* red = reinterpret_cast<float*>(smem + L::kOffRed);  // [2 parity][2 tile][2 half][128]
     auto red_at = [&](uint32_t par, int hh) { return red + ((par * 2 + x) * 2 + hh) * kM + t; };
     uint32_t c = 0, ni = 0, g = 0, xc = 0;  // xc: exchange-buffer uses
-    for (uint32_t n = 0;; ++n) {
-      const int it = next_item(n);
-      if (it < 0) break;
-      const Item item = load_item(items + it);
-      const int ntok = item.ntok;
-      const int ntiles = (ntok + kN - 1) / kN;
-      if (x == 1 && item.nrows <= kM) {
-        g += ntiles;
-        continue;  // tile B idle for this item
-      }
-      const int hd = item.kvh;
-      const int r = x * kM + t;  // row within the item
-      const bool live = r < item.nrows;
-      const int row = item.row0 + r;
-      const int qi = live ? row / G : 0;
-      const int qid = live ? __ldg(plan.pack_q + item.qoff + qi) : 0;
-      const int head = hd * G + (live ? row % G : 0);
-      const int slot = live ? __ldg(plan.unit_slot + item.slot_off + qi) : -1;
-
-      // Q row half -> smem (after the previous item's last QK of this tile)
-      mbar_wait(bar(Q_EMPTY + x), (ni & 1) ^ 1);
-      {
-        const uint4* src = reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + head) * D);
-        constexpr int kCh = D / 16;  // 16-byte chunks per half row
+    const int r = x * kM + t;                // row within an item
+    constexpr int kCh = D / 16;              // 16-byte chunks per half row
+    // Item n stays in its ring slot until this warp releases it after the
+    // epilogue, so per-item fields are re-read from shared memory where used
+    // instead of occupying registers across the KV loop.
+    auto wait_item = [&](uint32_t n) -> const ItemSlot* {
+      mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1);
+      return ring + (n & 1);
+    };
+    auto release_item = [&](uint32_t n) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
+    };
+    auto x_live = [&](const ItemSlot* s) { return x == 0 || s->item.nrows > kM; };
+    // cp.async this thread's half Q row of the slot's item into the swizzled
+    // Q tile (zero-filled for rows past the item).
+    auto issue_q = [&](const ItemSlot* s) {
+      const bool lv = r < s->item.nrows;
+      const int head = s->item.kvh * G + (lv ? (s->item.row0 + r) % G : 0);
+      const T* srcq = qg + ((int64_t)(lv ? s->meta[r].x : 0) * H + head) * D;
 #pragma unroll
-        for (int i = 0; i < kCh; ++i) {
-          const int ch = h * kCh + i;
-          uint4 v = live ? __ldg(src + ch) : make_uint4(0, 0, 0, 0);
-          st_shared_v4(sQ(x) + (ch >> 3) * (kM * 128) + t * 128 + (((ch & 7) ^ (t & 7)) << 4), v);
-        }
+      for (int i = 0; i < kCh; ++i) {
+        const int ch = h * kCh + i;
+        cp_async16(sQ(x) + (ch >> 3) * (kM * 128) + t * 128 + (((ch & 7) ^ (t & 7)) << 4), srcq + ch * 8, lv);
       }
+    };
+    auto finish_q = [&]() {
+      cp_async_wait_all();
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(Q_FULL + x));
+      if (t == 0 && h == 0) TC_TRACE(2 + x, 4, g);
+    };
+    bool q_pending = false;  // Q of the next x-live item issued, Q_FULL not yet arrived
+    {
+      const ItemSlot* s0 = wait_item(0);
+      if (s0->idx >= 0 && x_live(s0)) {
+        mbar_wait(bar(Q_EMPTY + x), (ni & 1) ^ 1);
+        issue_q(s0);
+        q_pending = true;
+      }
+    }
+    for (uint32_t n = 0;; ++n) {
+      const ItemSlot* cs = ring + (n & 1);  // ITEM_FULL(n) already waited
+      if (cs->idx < 0) break;
+      const int ntok = cs->item.ntok;
+      const int ntiles = (ntok + kN - 1) / kN;
+      if (!x_live(cs)) {
+        // tile B idle for this item; prefetch Q if the next item uses it
+        g += ntiles;
+        const ItemSlot* ns = wait_item(n + 1);
+        if (ns->idx >= 0 && x_live(ns)) {
+          mbar_wait(bar(Q_EMPTY + x), (ni & 1) ^ 1);
+          issue_q(ns);
+          q_pending = true;
+        }
+        release_item(n);
+        continue;
+      }
+      if (q_pending) {
+        finish_q();
+        q_pending = false;
+      }
 
       float m_ref = -INFINITY;  // running max, log2 units
       float2 l2 = make_float2(0.f, 0.f);
@@ -429,6 +493,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(S_EMPTY + x));
+        if (j == ntiles - 1) {
+          // last KV tile: this item's last QK is done, so the Q tile is free --
+          // start copying the next item's Q rows now
+          const ItemSlot* ns = wait_item(n + 1);
+          if (ns->idx >= 0 && x_live(ns)) {
+            mbar_wait(bar(Q_EMPTY + x), ni & 1);
+            issue_q(ns);
+            q_pending = true;
+          }
+        }
 
         const int valid = ntok - j * kN - 32 * h;  // valid columns of this half
         if (valid < 32) {
@@ -468,35 +542,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           l2.y *= alpha;
           m_ref = m_new;
         }
-        // P = exp2(s * scale - m_ref), packed 16-bit pairs (hi: 16 cols, lo: 16 cols)
+        // P = exp2(s * scale - m_ref), packed 16-bit pairs (hi: 16 cols, lo: 16
+        // cols), computed and stored in two chunks of 16 columns
         const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_ref, -m_ref);
-        uint32_t ph[16], pl[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          float2 a = __ffma2_rn(make_float2(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sc2, nm2);
-          a.x = ex2_approx(a.x);
-          a.y = ex2_approx(a.y);
-          ph[k] = Fmt<T>::pack(a.x, a.y);
-          if constexpr (kSplit) {
-            const float2 hf = make_float2(__uint_as_float(ph[k] << 16), __uint_as_float(ph[k] & 0xffff0000u));
-            const float2 lo = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
-            pl[k] = Fmt<T>::pack(lo.x, lo.y);
-            l2 = __fadd2_rn(l2, a);
-          } else {
-            // normalise by the sum of the ROUNDED weights the MMA actually uses:
-            // the output is then an exact weighted average of V rows
-            l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
+        for (int q2 = 0; q2 < 2; ++q2) {
+          uint32_t ph[8], pl[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int kk = q2 * 8 + k;
+            float2 a = __ffma2_rn(make_float2(__uint_as_float(sr[2 * kk]), __uint_as_float(sr[2 * kk + 1])), sc2, nm2);
+            a.x = ex2_approx(a.x);
+            a.y = ex2_approx(a.y);
+            ph[k] = Fmt<T>::pack(a.x, a.y);
+            if constexpr (kSplit) {
+              const float2 hf = make_float2(__uint_as_float(ph[k] << 16), __uint_as_float(ph[k] & 0xffff0000u));
+              const float2 lo = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
+              pl[k] = Fmt<T>::pack(lo.x, lo.y);
+              l2 = __fadd2_rn(l2, a);
+            } else {
+              // normalise by the sum of the ROUNDED weights the MMA actually uses:
+              // the output is then an exact weighted average of V rows
+              l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
+            }
           }
+          if (q2 == 0) {
+            if (t == 0 && h == 0) TC_TRACE(2 + x, 1, g);
+            // the P columns are free once PV of the previous tile completed
+            if (j > 0) {
+              mbar_wait(bar(O_DONE + x), (c - 1) & 1);
+              tc_fence_after();
+            }
+            if (t == 0 && h == 0) TC_TRACE(2 + x, 2, g);
+          }
+          tmem_st8(tP(x) + lane_base + 16 * h + 8 * q2, ph);
+          if constexpr (kSplit) tmem_st8(tP(x) + lane_base + 32 + 16 * h + 8 * q2, pl);
         }
-        if (t == 0 && h == 0) TC_TRACE(2 + x, 1, g);
-        // the P columns are free once PV of the previous tile completed
-        if (j > 0) {
-          mbar_wait(bar(O_DONE + x), (c - 1) & 1);
-          tc_fence_after();
-        }
-        if (t == 0 && h == 0) TC_TRACE(2 + x, 2, g);
-        tmem_st16(tP(x) + lane_base + 16 * h, ph);
-        if constexpr (kSplit) tmem_st16(tP(x) + lane_base + 32 + 16 * h, pl);
         if (j * kN + kN > ntok) {
           // tail tile: zero V rows past the span (both tiles may do it: same zeros)
           const int vt = ntok - j * kN;
@@ -517,12 +598,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t == 0 && h == 0) TC_TRACE(2 + x, 3, g);
       }
 
+      // the next item's first QK can now overlap this epilogue
+      if (q_pending) {
+        finish_q();
+        q_pending = false;
+      }
       // epilogue: O / l; the halves exchange their partial l
       float lh = l2.x + l2.y;
       *red_at(xc & 1, h) = lh;
       named_bar_sync(pair_bar, 64);
       const float l = lh + *red_at(xc & 1, h ^ 1);
       ++xc;
+      const bool live = r < cs->item.nrows;
+      const int2 meta = live ? cs->meta[r] : make_int2(0, -1);
+      const int head = cs->item.kvh * G + (live ? (cs->item.row0 + r) % G : 0);
       mbar_wait(bar(O_DONE + x), (c - 1) & 1);
       tc_fence_after();
       const float inv = 1.f / l;
@@ -532,8 +621,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int col = h * (D / 2) + q * 16;
         tmem_ld16(tO(x) + lane_base + (uint32_t)col, o);
         if (live) {
-          if (slot < 0) {
-            uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)qid * H + head) * D + col);
+          if (meta.y < 0) {
+            uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)meta.x * H + head) * D + col);
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const float* f = reinterpret_cast<const float*>(o + k * 8);
@@ -541,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   Fmt<T>::pack(f[4] * inv, f[5] * inv), Fmt<T>::pack(f[6] * inv, f[7] * inv));
             }
           } else {
-            float4* dst = reinterpret_cast<float4*>(part_o + ((int64_t)slot * H + head) * D + col);
+            float4* dst = reinterpret_cast<float4*>(part_o + ((int64_t)meta.y * H + head) * D + col);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const float* f = reinterpret_cast<const float*>(o + k * 4);
@@ -550,10 +639,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (live && slot >= 0 && h == 0) part_lse[(int64_t)slot * H + head] = m_ref + log2f(l);
+      if (live && meta.y >= 0 && h == 0) part_lse[(int64_t)meta.y * H + head] = m_ref + log2f(l);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(O_EMPTY + x));
+      if (t == 0 && h == 0) TC_TRACE(2 + x, 5, g - 1);
+      release_item(n);
       ++ni;
     }
   }

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--steps", type=int, default=24)
     ap.add_argument("--lib", default=TRACE_LIB)
     ap.add_argument("--dtype", default="bfloat16")
+    ap.add_argument("--config", default=None, help="trace CTA 0 of a BASELINE config layer instead")
     args = ap.parse_args()
     if args.build:
         from paper_2511_22333_b200 import build as B
@@ -42,14 +43,22 @@ def main():
     import paper_2511_22333_b200 as P
     from paper_2511_22333_b200 import _native as N
 
-    bs, nq, G, KVH, ntok = 16, args.nq, args.G, args.kvh, args.ntok
-    H = G * KVH
-    nblk = ntok // bs
-    table = P.BlockTable([list(range(nblk)) for _ in range(nq)], [bs] * nq, bs)
-    plan = P.PatPlan.from_table(table, H, KVH, 128, split="none", tc_min_rows=1)
-    inf = plan.info()
     dt = getattr(torch, args.dtype)
     g = torch.Generator(device="cuda").manual_seed(0)
+    if args.config:
+        from paper_2511_22333_b200 import configs
+        w = configs.workload(args.config)
+        table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+        plan = P.PatPlan.from_table(table, w.num_heads, w.num_kv_heads, w.head_dim, split="native")
+        nq, H, KVH, ntok, nblk, bs = w.batch, w.num_heads, w.num_kv_heads, 0, w.num_pool_blocks(), w.block_size
+        G = H // KVH
+    else:
+        bs, nq, G, KVH, ntok = 16, args.nq, args.G, args.kvh, args.ntok
+        H = G * KVH
+        nblk = ntok // bs
+        table = P.BlockTable([list(range(nblk)) for _ in range(nq)], [bs] * nq, bs)
+        plan = P.PatPlan.from_table(table, H, KVH, 128, split="none", tc_min_rows=1)
+    inf = plan.info()
     kc = torch.randn(nblk, bs, KVH, 128, device="cuda", dtype=dt, generator=g)
     vc = torch.randn(nblk, bs, KVH, 128, device="cuda", dtype=dt, generator=g)
     q = torch.randn(nq, H, 128, device="cuda", dtype=dt, generator=g)
@@ -75,18 +84,20 @@ def main():
     lib.pat_debug_tc_trace.argtypes = [C.c_void_p]
     assert lib.pat_debug_tc_trace(tr.ctypes.data) == 0
     t0 = tr[0, 0, 0]
-    names = {(0, 0): "prod_kvempty", (1, 0): "mma_kvfull", (1, 3): "qkA_start", (1, 1): "mma_qk_issued",
+    names = {(0, 0): "prod_kvempty", (1, 5): "mma_item_qfull", (1, 0): "mma_kvfull", (1, 3): "qkA_start",
+             (1, 1): "mma_qk_issued",
              (1, 4): "pvA_start(j-1)", (1, 2): "mma_pv_issued",
-             (2, 0): "smA_sfull", (2, 1): "smA_exp_done", (2, 2): "smA_odone", (2, 3): "smA_pfull",
+             (2, 4): "smA_qstored", (2, 0): "smA_sfull", (2, 1): "smA_exp_done", (2, 2): "smA_odone",
+             (2, 3): "smA_pfull", (2, 5): "smA_epi_done",
              (3, 0): "smB_sfull", (3, 1): "smB_exp_done", (3, 2): "smB_odone", (3, 3): "smB_pfull"}
-    hdr = " step " + " ".join(f"{v:>14s}" for v in names.values())
+    hdr = " step " + " ".join(f"{v:>15s}" for v in names.values())
     print(hdr)
-    n = min(args.steps, ntok // 64)
+    n = min(args.steps, ntok // 64) if ntok else args.steps
     for s in range(n):
         row = []
         for (r, e) in names:
             v = tr[r, e, s]
-            row.append(f"{(v - t0) if v else -1:>14d}")
+            row.append(f"{(v - t0) if v else -1:>15d}")
         print(f"{s:5d} " + " ".join(row))
     # steady-state per-step cycles from the MMA issuer's KV_FULL timestamps
     m = tr[1, 0, :n]
