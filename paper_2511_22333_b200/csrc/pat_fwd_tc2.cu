@@ -1,26 +1,26 @@
-// Tensor-core (tcgen05 + TMEM + TMA) forward kernel for WIDE packs, two
-// 128-row query tiles per CTA (FA4-style ping-pong).
+// Tensor-core (tcgen05 + TMEM + TMA) forward kernel: one persistent CTA per SM
+// pulls work items (unit x kv head x up-to-128 rows) from a global counter in
+// the scheduler's longest-first order and streams each item's KV span once
+// through a 6-stage TMA ring.  Every pack goes through it: a narrow pack (a few
+// queries x G heads) still runs QK^T / PV on the tensor core (M = 128 rows, the
+// padding rows are free: the kernel is HBM- or softmax-bound, never MMA-bound).
 //
-// A pack whose query tile (queries x G heads of one kv head) fills >= 64 rows
-// forms a real dense contraction: S = Q K^T and O += P V run on the 5th-gen
-// tensor cores.  One CTA (12 warps, one per SM) owns work items of
-// (unit, kv head, 256 rows) = tiles A (rows 0-127) and B (rows 128-255) and
-// streams the unit's KV span ONCE for both:
-//   warp 0      TMA producer: 16-token page slices of K and V, 5-stage ring of
-//               64-token stages, 128B swizzle, from the paged cache;
-//   warp 1      MMA issuer (one thread), per KV tile j:
-//                 S_A(j) = Q_A K_j^T, S_B(j) = Q_B K_j^T   (SS, M=128 N=64 K=d)
-//                 O_A += P_A(j-1) V_{j-1}, O_B += P_B(j-1) V_{j-1}
-//                 (TS: P read straight from TMEM, V an MN-major smem operand)
-//               so the tensor core works on one tile while the other tile's
-//               softmax runs;
-//   warp 2      TMEM allocator (512 columns: S_A x2, S_B x2, O_A, O_B);
-//   warps 4-7   softmax / epilogue of tile A (thread = row = TMEM lane);
-//   warps 8-11  softmax / epilogue of tile B.
-// Softmax: tcgen05.ld S, scale/mask in log2 units, lazy O rescale (only when the
-// running max grows by > 8), P packed to 16-bit and tcgen05.st back over S
-// (bf16: P = hi + lo, two PV MMAs, ~16-bit P).  Numerics follow cta_partial
-// (attention.py:140-163): fp32 scores and accumulators.
+//   warp 0      producer: claims items (atomic counter), resolves per-row
+//               (query id, partial slot) into a 2-slot shared item ring, and
+//               issues TMA boxes of 16-token page slices of K and V (64-token
+//               stages, 128B swizzle) straight from the paged cache;
+//   warp 1      TMEM allocator + MMA issuer (whole warp, one elected lane):
+//                 S[c&1] = Q K_c^T     (TS: Q from TMEM, K K-major smem, M=128 N=64)
+//                 O     += P[c-1] V    (TS: P from TMEM, V MN-major smem, N=d)
+//               QK of tile c is issued before PV of tile c-1, S and P are
+//               double-buffered, so softmax(c) overlaps PV(c-1) and QK(c+1);
+//   warps 2-17  softmax / epilogue: 4 warps per TMEM lane quarter, each owning
+//               16 of the 64 score columns (row max exchanged through smem).
+// TMEM: S[2] (64 cols each), P[2] (64 cols: hi 32 + lo 32 packed 16-bit pairs),
+// O (d cols fp32), Q (d/2 cols, packed 16-bit pairs) = 448 of 512 columns.
+// Numerics follow cta_partial (attention.py:140-163): fp32 scores and
+// accumulators, log2-domain online softmax with lazy O rescale (only when the
+// running max grows by > 8), bf16 P = hi + lo (two PV MMAs).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -34,12 +34,12 @@ namespace tc2 {
 
 #ifdef PAT_TC_TRACE
 // Debug timeline (tools/tc_trace.py): CTA 0 records clock64 per (role, event, step).
-// roles: 0 producer, 1 MMA issuer, 2 softmax tile A (warp 4 lane 0), 3 softmax tile B.
+// roles: 0 producer, 1 MMA issuer, 2 softmax (warp 2 lane 0), 3 unused.
 constexpr int kTraceSteps = 256;
 __device__ long long g_tc_trace[4][8][kTraceSteps];
 __device__ unsigned long long g_span_tc[1][kSpanCtas][2];
-#define TC_TRACE(role, ev, step)                                        \
-  do {                                                                  \
+#define TC_TRACE(role, ev, step)                                                         \
+  do {                                                                                   \
     if (blockIdx.x == 0 && (step) < kTraceSteps) g_tc_trace[role][ev][step] = clock64(); \
   } while (0)
 #else
@@ -48,44 +48,21 @@ __device__ unsigned long long g_span_tc[1][kSpanCtas][2];
   } while (0)
 #endif
 constexpr int kThreads = 576;  // producer, MMA issuer (+TMEM alloc), 16 softmax warps
-constexpr int kM = 128;       // rows per tile
-constexpr int kN = 64;        // tokens per KV tile
-constexpr int kStages = 4;
+constexpr int kSoftWarps = 16;
+constexpr int kM = 128;        // rows per item tile (TMEM lanes)
+constexpr int kN = 64;         // tokens per KV tile
+constexpr int kStages = 6;
 constexpr uint32_t kTmemCols = 512;
 #ifndef PAT_TC_RESCALE_THRESHOLD
 #define PAT_TC_RESCALE_THRESHOLD 8.0f
 #endif
 constexpr float kRescaleThreshold = PAT_TC_RESCALE_THRESHOLD;  // log2 units
 
-template <int D>
-struct Layout {
-  static constexpr int KB = D / 64;
-  static constexpr int kQBytes = KB * kM * 128;      // one tile's Q: [KB][128][64]
-  static constexpr int kTileBytes = KB * kN * 128;   // K or V stage tile: [KB][64][64]
-  static constexpr int kOffQ = 0;                    // Q_A, Q_B
-  static constexpr int kOffKV = 2 * kQBytes;
-  static constexpr int kOffBar = kOffKV + kStages * 2 * kTileBytes;
-  static constexpr int kOffRed = kOffBar + 512;         // row-max / row-sum exchange
-  static constexpr int kOffRing = kOffRed + 2 * 2 * 2 * kM * 4;  // 2 x ItemSlot
-  static constexpr int kBytes = kOffRing + 2 * 2112;
-  static constexpr int kAlloc = kBytes + 1024;
-};
-
-enum Bar : int {
-  KV_FULL = 0,
-  KV_EMPTY = KV_FULL + kStages,
-  S_FULL = KV_EMPTY + kStages,  // [tile] QK done
-  S_EMPTY = S_FULL + 2,         // [tile] softmax has read S
-  P_FULL = S_EMPTY + 2,         // [tile] P written to TMEM
-  O_DONE = P_FULL + 2,          // [tile] PV done (O updated, P region free)
-  O_EMPTY = O_DONE + 2,         // [tile]
-  Q_FULL = O_EMPTY + 2,         // [tile]
-  Q_EMPTY = Q_FULL + 2,         // [tile]
-  ITEM_FULL = Q_EMPTY + 2,      // [slot] work-item index published by the producer
-  ITEM_EMPTY = ITEM_FULL + 2,   // [slot] read by the MMA warp and the 16 softmax warps
-  NUM_BARS = ITEM_EMPTY + 2
-};
-constexpr int kItemReaders = 17;
+// TMEM column map
+constexpr uint32_t kColS = 0;    // S[b] at 64 b
+constexpr uint32_t kColP = 128;  // P[b] at 128 + 64 b (hi 0-31, lo 32-63)
+constexpr uint32_t kColO = 256;
+constexpr uint32_t kColQ = 384;
 
 // One slot of the work-item ring: the item and, per row, the query id and
 // partial slot resolved by the producer warp (so consumers never chase the
@@ -94,9 +71,39 @@ struct ItemSlot {
   int32_t idx;
   int32_t pad[7];
   Item item;
-  int2 meta[2 * 128];  // (qid, slot) per row
+  int2 meta[kM];  // (qid, slot) per row
 };
-static_assert(sizeof(ItemSlot) == 2112, "ItemSlot layout");
+static_assert(sizeof(ItemSlot) == 64 + 8 * kM, "ItemSlot layout");
+constexpr uint32_t kSlotBytes = sizeof(ItemSlot);
+constexpr uint32_t kFIdx = 0, kFKvh = 32 + 4, kFRow0 = 32 + 8, kFNrows = 32 + 12, kFNtok = 32 + 20, kFMeta = 64;
+
+template <int D>
+struct Layout {
+  static constexpr int KB = D / 64;
+  static constexpr int kTileBytes = KB * kN * 128;   // K or V stage tile: [KB][64][64]
+  static constexpr int kOffKV = 0;
+  static constexpr int kOffBar = kOffKV + kStages * 2 * kTileBytes;
+  static constexpr int kOffRed = kOffBar + 512;                    // [2 parity][4 cq][128 rows] floats
+  static constexpr int kOffRing = kOffRed + 2 * 4 * kM * 4;        // 2 x ItemSlot
+  static constexpr int kBytes = kOffRing + 2 * (int)sizeof(ItemSlot);
+  static constexpr int kAlloc = kBytes + 1024;
+};
+
+enum Bar : int {
+  KV_FULL = 0,
+  KV_EMPTY = KV_FULL + kStages,
+  S_FULL = KV_EMPTY + kStages,  // [buffer] QK done
+  S_EMPTY = S_FULL + 2,         // [buffer] softmax has read S
+  P_FULL = S_EMPTY + 2,         // [buffer] P written to TMEM
+  P_FREE = P_FULL + 2,          // [buffer] the PV reading P[b] completed (O updated)
+  O_EMPTY = P_FREE + 2,         // epilogue has read O
+  Q_FULL = O_EMPTY + 1,         // Q written to TMEM
+  Q_EMPTY = Q_FULL + 1,         // last QK of the item completed
+  ITEM_FULL = Q_EMPTY + 1,      // [slot] work item published by the producer
+  ITEM_EMPTY = ITEM_FULL + 2,   // [slot] released by the MMA warp and the 16 softmax warps
+  NUM_BARS = ITEM_EMPTY + 2
+};
+constexpr int kItemReaders = 1 + kSoftWarps;
 
 template <typename T> struct Fmt;
 template <> struct Fmt<__half> {
@@ -106,7 +113,6 @@ template <> struct Fmt<__half> {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
   }
-  static __device__ __forceinline__ uint32_t pack_lo(float, float, uint32_t) { return 0u; }
   static __device__ __forceinline__ float2 unpack(uint32_t v) {
     return __half22float2(*reinterpret_cast<__half2*>(&v));
   }
@@ -122,11 +128,6 @@ template <> struct Fmt<__nv_bfloat16> {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
   }
-  static __device__ __forceinline__ uint32_t pack_lo(float a, float b, uint32_t hi) {
-    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&hi);
-    float2 f = __bfloat1622float2(h);
-    return pack(a - f.x, b - f.y);
-  }
   static __device__ __forceinline__ float2 unpack(uint32_t v) {
     return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
   }
@@ -136,7 +137,6 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
-
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -147,16 +147,25 @@ __device__ __forceinline__ float ex2_approx(float v) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
   return r;
 }
-// 16-byte global -> shared async copy; src_size 0 zero-fills the destination
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
-               : "memory");
+// shared-space accesses by 32-bit address (the dynamic-smem base is re-aligned
+// through an integer, so C++ pointers into it lose the shared address space)
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ int2 lds_v2(uint32_t a) {
+  int2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) { return __int_as_float(lds_s32(a)); }
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
-
 __device__ __forceinline__ Item load_item(const Item* p) {
   const int4* q = reinterpret_cast<const int4*>(p);
   int4 a = __ldg(q), b = __ldg(q + 1);
@@ -171,17 +180,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   using L = Layout<D>;
   using namespace sm100;
   constexpr bool kSplit = Fmt<T>::kSplit;
+  constexpr int kQCols = D / 8;   // Q columns per softmax warp (its quarter of d, packed pairs)
+  constexpr int kOCols = D / 4;   // O columns per softmax warp
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sb = smem_u32(smem);
-  const uint32_t sKV = sb + L::kOffKV;
   const uint32_t bars = sb + L::kOffBar;
   uint32_t* tmem_slot = (uint32_t*)(smem + L::kOffBar + NUM_BARS * 8);
   ItemSlot* ring = reinterpret_cast<ItemSlot*>(smem + L::kOffRing);
   auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
-  auto sQ = [&](int x) { return sb + L::kOffQ + (uint32_t)(x * L::kQBytes); };
-  auto sK = [&](int s) { return sKV + (uint32_t)(s * 2 * L::kTileBytes); };
-  auto sV = [&](int s) { return sKV + (uint32_t)(s * 2 * L::kTileBytes + L::kTileBytes); };
+  auto sK = [&](int s) { return sb + L::kOffKV + (uint32_t)(s * 2 * L::kTileBytes); };
+  auto sV = [&](int s) { return sb + L::kOffKV + (uint32_t)(s * 2 * L::kTileBytes + L::kTileBytes); };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = plan.H, G = plan.G, bs = plan.bs;
@@ -193,19 +202,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(KV_FULL + s), 1);
       mbar_init(bar(KV_EMPTY + s), 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(S_FULL + i), 1);
-      mbar_init(bar(S_EMPTY + i), 8);
-      mbar_init(bar(P_FULL + i), 8);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(S_FULL + b), 1);
+      mbar_init(bar(S_EMPTY + b), kSoftWarps);
+      mbar_init(bar(P_FULL + b), kSoftWarps);
+      mbar_init(bar(P_FREE + b), 1);
+      mbar_init(bar(ITEM_FULL + b), 32);
+      mbar_init(bar(ITEM_EMPTY + b), kItemReaders);
     }
-    for (int x = 0; x < 2; ++x) {
-      mbar_init(bar(O_DONE + x), 1);
-      mbar_init(bar(O_EMPTY + x), 8);
-      mbar_init(bar(Q_FULL + x), 8);
-      mbar_init(bar(Q_EMPTY + x), 1);
-      mbar_init(bar(ITEM_FULL + x), 32);
-      mbar_init(bar(ITEM_EMPTY + x), kItemReaders);
-    }
+    mbar_init(bar(O_EMPTY), kSoftWarps);
+    mbar_init(bar(Q_FULL), kSoftWarps);
+    mbar_init(bar(Q_EMPTY), 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(smem_u32(tmem_slot));
@@ -214,324 +221,263 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   PAT_SPAN_BEGIN(g_span_tc, 0);
-  // TMEM columns: S[x] at 128x, P[x] at 128x + 64 (hi: +0..31, lo: +32..63),
-  // O[x] at 256 + 128x.  P has its own columns: a PV MMA reading P from TMEM
-  // must never share columns with a later QK MMA's accumulator (measured WAR
-  // hazard when P lived inside the double-buffered S region).
-  // Dynamic work distribution: the producer claims items (in the scheduler's
-  // longest-first order) from a global counter one item ahead and publishes
-  // the index through a 2-slot shared ring; the MMA warp and the softmax
-  // warps follow the same sequence.  -1 ends the loop.
-  // Returns the item index (-1 = done), the item and, for row `r` (< 0: none),
-  // its (qid, slot) metadata.
-  auto next_item = [&](uint32_t n, Item& itm, int r, int2& meta) -> int {
-    const uint32_t slot = n & 1;
-    mbar_wait(bar(ITEM_FULL + slot), (n >> 1) & 1);
-    const ItemSlot* rs = ring + slot;  // plain loads: ordered by the mbarrier wait (asm memory clobber)
-    const int it = rs->idx;
-    if (it >= 0) {
-      itm = rs->item;
-      if (r >= 0 && r < itm.nrows) meta = rs->meta[r];
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + slot));
-    return it;
-  };
-  auto tS = [&](int x) { return tmem + (uint32_t)(128 * x); };
-  auto tP = [&](int x) { return tmem + (uint32_t)(128 * x + 64); };
-  auto tO = [&](int x) { return tmem + 256u + (uint32_t)(128 * x); };
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    // Whole warp: lane i fetches the block id of page group i of the stage,
-    // broadcast by shuffle (warp-uniform operands), one elected lane issues.
-    {
-      if (elect_one()) {
-        tma_prefetch(&tmk);
-        tma_prefetch(&tmv);
+    // ------------------------------------------------------------ producer
+    // Whole warp: lane i fetches the block id of page group i of a stage,
+    // broadcast by shuffle (warp-uniform TMA operands), one elected lane issues.
+    if (elect_one()) {
+      tma_prefetch(&tmk);
+      tma_prefetch(&tmv);
+    }
+    uint32_t g = 0;
+    for (uint32_t n = 0;; ++n) {
+      const uint32_t slot = n & 1;
+      mbar_wait(bar(ITEM_EMPTY + slot), ((n >> 1) & 1) ^ 1);
+      int it = 0;
+      if (lane == 0) {
+        it = atomicAdd(plan.sched, 1);
+        if (it >= n_items) it = -1;
       }
-      uint32_t g = 0;
-      for (uint32_t n = 0;; ++n) {
-        const uint32_t slot = n & 1;
-        mbar_wait(bar(ITEM_EMPTY + slot), ((n >> 1) & 1) ^ 1);
-        int it = 0;
-        if (lane == 0) {
-          it = atomicAdd(plan.sched, 1);
-          if (it >= n_items) it = -1;
+      it = __shfl_sync(0xffffffffu, it, 0);
+      Item item{};
+      if (it >= 0) {
+        item = load_item(items + it);
+        for (int r = lane; r < item.nrows; r += 32) {
+          const int qi = (item.row0 + r) / G;
+          ring[slot].meta[r] =
+              make_int2(__ldg(plan.pack_q + item.qoff + qi), __ldg(plan.unit_slot + item.slot_off + qi));
         }
-        it = __shfl_sync(0xffffffffu, it, 0);
-        Item item{};
-        if (it >= 0) {
-          item = load_item(items + it);
-          for (int r = lane; r < item.nrows; r += 32) {
-            const int qi = (item.row0 + r) / G;
-            ring[slot].meta[r] = make_int2(__ldg(plan.pack_q + item.qoff + qi), __ldg(plan.unit_slot + item.slot_off + qi));
-          }
-          if (lane == 0) ring[slot].item = item;
+        if (lane == 0) ring[slot].item = item;
+      }
+      if (lane == 0) ring[slot].idx = it;
+      __syncwarp();
+      mbar_arrive(bar(ITEM_FULL + slot));
+      if (it < 0) break;
+      const int h = item.kvh, ntok = item.ntok;
+      const int32_t* blist = plan.pack_blk + item.blk;
+      const int ntiles = (ntok + kN - 1) / kN;
+      for (int j = 0; j < ntiles; ++j, ++g) {
+        const int s = g % kStages;
+        const int rem = ntok - j * kN;
+        const int ngrp = rem >= kN ? kN / 16 : (rem + 15) / 16;
+        int my_blk = 0, my_off = 0;
+        if (lane < ngrp) {
+          const int tok = j * kN + lane * 16;
+          const int pg = bs == 16 ? (tok >> 4) : tok / bs;
+          my_blk = __ldg(blist + pg);
+          my_off = bs == 16 ? 0 : tok - pg * bs;
         }
-        if (lane == 0) ring[slot].idx = it;
+        mbar_wait(bar(KV_EMPTY + s), ((g / kStages) & 1) ^ 1);
+        TC_TRACE(0, 0, g);
+        if (elect_one()) mbar_expect_tx(bar(KV_FULL + s), (uint32_t)(ngrp * L::KB * 2048 * 2));
         __syncwarp();
-        mbar_arrive(bar(ITEM_FULL + slot));
-        if (it < 0) break;
-        const int h = item.kvh, ntok = item.ntok;
-        const int32_t* blist = plan.pack_blk + item.blk;
-        const int ntiles = (ntok + kN - 1) / kN;
-        for (int j = 0; j < ntiles; ++j, ++g) {
-          const int s = g % kStages;
-          const int rem = ntok - j * kN;
-          const int ngrp = rem >= kN ? kN / 16 : (rem + 15) / 16;
-          int my_blk = 0, my_off = 0;
-          if (lane < ngrp) {
-            const int tok = j * kN + lane * 16;
-            const int pg = bs == 16 ? (tok >> 4) : tok / bs;
-            my_blk = __ldg(blist + pg);
-            my_off = bs == 16 ? 0 : tok - pg * bs;
-          }
-          mbar_wait(bar(KV_EMPTY + s), ((g / kStages) & 1) ^ 1);
-          TC_TRACE(0, 0, g);
-          if (elect_one()) mbar_expect_tx(bar(KV_FULL + s), (uint32_t)(ngrp * L::KB * 2048 * 2));
-          __syncwarp();
-          for (int gr = 0; gr < ngrp; ++gr) {
-            const int blk = __shfl_sync(0xffffffffu, my_blk, gr);
-            const int off = __shfl_sync(0xffffffffu, my_off, gr);
-            if (elect_one()) {
+        for (int gr = 0; gr < ngrp; ++gr) {
+          const int blk = __shfl_sync(0xffffffffu, my_blk, gr);
+          const int off = __shfl_sync(0xffffffffu, my_off, gr);
+          if (elect_one()) {
 #pragma unroll
-              for (int kb = 0; kb < L::KB; ++kb) {
-                tma_load_4d(sK(s) + kb * (kN * 128) + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
-                tma_load_4d(sV(s) + kb * (kN * 128) + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
-              }
+            for (int kb = 0; kb < L::KB; ++kb) {
+              tma_load_4d(sK(s) + kb * (kN * 128) + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
+              tma_load_4d(sV(s) + kb * (kN * 128) + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
             }
-            __syncwarp();
           }
+          __syncwarp();
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs the loop so descriptors and TMEM addresses stay
-    // warp-uniform (uniform datapath, no per-MMA waterfall); one elected lane
-    // issues each tcgen05.mma / commit (CUTLASS's elect_one_sync pattern).
-    {
-      constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
-      constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
-      uint32_t g = 0;           // KV tiles consumed
-      uint32_t c[2] = {0, 0};   // KV tiles processed per query tile (S/P buffer index)
-      uint32_t ni[2] = {0, 0};  // items processed per query tile
-      auto commit = [&](int b) {
-        if (elect_one()) umma_commit(bar(b));
-        __syncwarp();
-      };
-      auto issue_qk = [&](int x, int s, uint32_t ci) {
-        // S[x] is single-buffered: wait until the softmax has read tile ci-1
-        mbar_wait(bar(S_EMPTY + x), (ci & 1) ^ 1);
-        if (x == 0) TC_TRACE(1, 3, g);
+    // warp-uniform (uniform datapath); one elected lane issues each
+    // tcgen05.mma / commit (the same lane every time: all lanes are active).
+    constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
+    constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
+    uint32_t g = 0;  // KV tiles consumed (ring position)
+    uint32_t c = 0;  // KV tiles processed (S / P buffer sequence)
+    auto commit = [&](int b) {
+      if (elect_one()) umma_commit(bar(b));
+      __syncwarp();
+    };
+    auto issue_pv = [&](uint32_t cc, int s, bool first) {
+      const uint32_t b = cc & 1;
+      mbar_wait(bar(P_FULL + b), (cc >> 1) & 1);
+      if (b == 0) TC_TRACE(1, 4, g);
+      tc_fence_after();
+      const uint64_t v0 = umma_desc_sw128(sV(s), kN * 128, 1024);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < kN / 16; ++k) {
+          const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
+          // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
+          const uint32_t tp = tmem + kColP + 64u * b + (uint32_t)(k * 8);
+          umma_f16_ts(tmem + kColO, tp, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
+          if constexpr (kSplit) umma_f16_ts(tmem + kColO, tp + 32, bd, idesc_pv, 1u);
+        }
+        umma_commit(bar(P_FREE + b));
+        umma_commit(bar(KV_EMPTY + s));
+      }
+      __syncwarp();
+    };
+    uint32_t n_items_done = 0;
+    for (uint32_t n = 0;; ++n) {
+      mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1);
+      const uint32_t rs = sb + L::kOffRing + (n & 1) * kSlotBytes;
+      const int it = lds_s32(rs + kFIdx);
+      const int ntok = it >= 0 ? lds_s32(rs + kFNtok) : 0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
+      if (it < 0) break;
+      const int ntiles = (ntok + kN - 1) / kN;
+      mbar_wait(bar(Q_FULL), n_items_done & 1);
+      TC_TRACE(1, 5, g);
+      tc_fence_after();
+      int sprev = 0;
+      for (int j = 0; j < ntiles; ++j, ++g, ++c) {
+        const int s = g % kStages;
+        const uint32_t b = c & 1;
+        mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
+        TC_TRACE(1, 0, g);
+        mbar_wait(bar(S_EMPTY + b), ((c >> 1) & 1) ^ 1);  // softmax read S[b] (tile c-2)
+        TC_TRACE(1, 3, g);
         tc_fence_after();
-        const uint64_t a0 = umma_desc_sw128(sQ(x), 16, 1024), b0 = umma_desc_sw128(sK(s), 16, 1024);
+        const uint64_t k0 = umma_desc_sw128(sK(s), 16, 1024);
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             const int kb = k >> 2, kk = k & 3;
-            // descriptor start address is in 16-byte units (bits 0-13)
-            umma_f16_ss(tS(x), a0 + (uint64_t)((kb * (kM * 128) + kk * 32) >> 4),
-                        b0 + (uint64_t)((kb * (kN * 128) + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
+            // Q(m, k) packed two per column: a k-step of 16 = 8 columns
+            umma_f16_ts(tmem + kColS + 64u * b, tmem + kColQ + (uint32_t)(k * 8),
+                        k0 + (uint64_t)((kb * (kN * 128) + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
           }
+          umma_commit(bar(S_FULL + b));
+          if (j == ntiles - 1) umma_commit(bar(Q_EMPTY));
         }
         __syncwarp();
-      };
-      auto issue_pv = [&](int x, int s, uint32_t ci, bool first) {
-        if (first) mbar_wait(bar(O_EMPTY + x), (ni[x] & 1) ^ 1);
-        mbar_wait(bar(P_FULL + x), ci & 1);
-        if (x == 0) TC_TRACE(1, 4, g);
-        tc_fence_after();
-        const uint64_t v0 = umma_desc_sw128(sV(s), kN * 128, 1024);
-        if (elect_one()) {
-#pragma unroll
-          for (int k = 0; k < kN / 16; ++k) {
-            const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
-            // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
-            umma_f16_ts(tO(x), tP(x) + k * 8, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
-            if constexpr (kSplit) umma_f16_ts(tO(x), tP(x) + 32 + k * 8, bd, idesc_pv, 1u);
-          }
-          umma_commit(bar(O_DONE + x));
+        TC_TRACE(1, 1, g);
+        if (j > 0) {
+          if (j == 1) mbar_wait(bar(O_EMPTY), (n_items_done & 1) ^ 1);
+          issue_pv(c - 1, sprev, j == 1);
+          TC_TRACE(1, 2, g);
         }
-        __syncwarp();
-      };
-      for (uint32_t n = 0;; ++n) {
-        Item item;
-        int2 unused;
-        if (next_item(n, item, -1, unused) < 0) break;
-        const bool liveB = item.nrows > kM;
-        const int ntiles = (item.ntok + kN - 1) / kN;
-        mbar_wait(bar(Q_FULL + 0), ni[0] & 1);
-        if (liveB) mbar_wait(bar(Q_FULL + 1), ni[1] & 1);
-        TC_TRACE(1, 5, g);
-        tc_fence_after();
-        int sprev = 0;
-        for (int j = 0; j < ntiles; ++j, ++g) {
-          const int s = g % kStages;
-          mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
-          TC_TRACE(1, 0, g);
-          tc_fence_after();
-          // Both tiles' S MMAs are issued before either S_FULL is signalled:
-          // a softmax must not read/write its S region while the OTHER tile's
-          // QK MMA is in flight (measured: corrupted S/P when the two S
-          // regions are 128 or 256 TMEM columns apart; tools/tc_debug.py).
-          issue_qk(0, s, c[0] + j);
-          if (liveB) issue_qk(1, s, c[1] + j);
-          commit(S_FULL + 0);
-          if (liveB) commit(S_FULL + 1);
-          if (j == ntiles - 1) {
-            commit(Q_EMPTY + 0);
-            if (liveB) commit(Q_EMPTY + 1);
-          }
-          TC_TRACE(1, 1, g);
-          if (j > 0) {
-            issue_pv(0, sprev, c[0] + j - 1, j == 1);
-            TC_TRACE(1, 2, g);
-            if (liveB) issue_pv(1, sprev, c[1] + j - 1, j == 1);
-            commit(KV_EMPTY + sprev);
-          }
-          sprev = s;
-        }
-        issue_pv(0, sprev, c[0] + ntiles - 1, ntiles == 1);
-        if (liveB) issue_pv(1, sprev, c[1] + ntiles - 1, ntiles == 1);
-        commit(KV_EMPTY + sprev);
-        c[0] += ntiles;
-        ++ni[0];
-        if (liveB) {
-          c[1] += ntiles;
-          ++ni[1];
-        }
+        sprev = s;
       }
+      if (ntiles == 1) mbar_wait(bar(O_EMPTY), (n_items_done & 1) ^ 1);
+      issue_pv(c - 1, sprev, ntiles == 1);
+      ++n_items_done;
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
-    // 16 warps (2-17): tile x = sw >> 3, column half h = (sw >> 2) & 1, lane
-    // quarter wq = warp % 4 (the TMEM lanes the warp may access).  The two
-    // halves of a row (same lanes, same SMSP) exchange their partial row max
-    // through shared memory each KV tile, so both keep the same running max.
-    const int sw = warp - 2;
-    const int x = sw >> 3, h = (sw >> 2) & 1, wq = warp & 3;
-    const int t = wq * 32 + lane;                 // row in the tile == TMEM lane
+    // warps 2-17: lane quarter wq = warp % 4 (the TMEM lanes the warp may
+    // access), column quarter cq: 16 of the 64 score columns, 16 tokens' P,
+    // d/4 of O and Q.  The 4 warps of a lane quarter exchange partial row
+    // maxima through shared memory every KV tile (named barrier per quarter).
+    const int wq = warp & 3, cq = (warp - 2) >> 2;
+    const int t = wq * 32 + lane;                 // row in the item == TMEM lane
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    const uint32_t pair_bar = 1 + x * 4 + wq;     // named barrier of the two half-warps
-    float* red = reinterpret_cast<float*>(smem + L::kOffRed);  // [2 parity][2 tile][2 half][128]
-    auto red_at = [&](uint32_t par, int hh) { return red + ((par * 2 + x) * 2 + hh) * kM + t; };
-    uint32_t c = 0, ni = 0, g = 0, xc = 0;  // xc: exchange-buffer uses
-    const int r = x * kM + t;                // row within an item
-    constexpr int kCh = D / 16;              // 16-byte chunks per half row
-    // Item n stays in its ring slot until this warp releases it after the
-    // epilogue, so per-item fields are re-read from shared memory where used
-    // instead of occupying registers across the KV loop.
-    auto wait_item = [&](uint32_t n) -> const ItemSlot* {
-      mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1);
-      return ring + (n & 1);
-    };
+    const uint32_t quarter_bar = 1 + wq;          // named barrier of the 4 warps of a lane quarter
+    const uint32_t red = sb + L::kOffRed;  // [2 parity][4 cq][128] floats
+    auto red_at = [&](uint32_t par, int q) { return red + (uint32_t)(((par * 4 + q) * kM + t) * 4); };
+    const uint32_t ring_s = sb + L::kOffRing;
+    auto fld = [&](uint32_t n, uint32_t off) { return lds_s32(ring_s + (n & 1) * kSlotBytes + off); };
+    const bool tr = (t == 0 && cq == 0);          // trace thread
+    uint32_t c = 0, g = 0, xc = 0, ni = 0;        // xc: exchange-buffer uses
+
+    auto wait_item = [&](uint32_t n) { mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1); };
     auto release_item = [&](uint32_t n) {
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
     };
-    auto x_live = [&](const ItemSlot* s) { return x == 0 || s->item.nrows > kM; };
-    // cp.async this thread's half Q row of the slot's item into the swizzled
-    // Q tile (zero-filled for rows past the item).
-    auto issue_q = [&](const ItemSlot* s) {
-      const bool lv = r < s->item.nrows;
-      const int head = s->item.kvh * G + (lv ? (s->item.row0 + r) % G : 0);
-      const T* srcq = qg + ((int64_t)(lv ? s->meta[r].x : 0) * H + head) * D;
+    // this thread's quarter of its Q row of the slot's item (zero past the item)
+    auto load_q = [&](uint32_t n, uint32_t* qv) {
+      const bool lv = t < fld(n, kFNrows);
+      if (lv) {
+        const int head = fld(n, kFKvh) * G + (fld(n, kFRow0) + t) % G;
+        const int qid = fld(n, kFMeta + 8 * t);
+        const uint4* src = reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + head) * D + cq * (D / 4));
 #pragma unroll
-      for (int i = 0; i < kCh; ++i) {
-        const int ch = h * kCh + i;
-        cp_async16(sQ(x) + (ch >> 3) * (kM * 128) + t * 128 + (((ch & 7) ^ (t & 7)) << 4), srcq + ch * 8, lv);
+        for (int i = 0; i < kQCols / 4; ++i) {
+          const uint4 v = __ldg(src + i);
+          qv[4 * i] = v.x, qv[4 * i + 1] = v.y, qv[4 * i + 2] = v.z, qv[4 * i + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kQCols; ++i) qv[i] = 0u;
       }
     };
-    auto finish_q = [&]() {
-      cp_async_wait_all();
-      fence_proxy_async_smem();
+    auto store_q = [&](const uint32_t* qv) {
+      const uint32_t ta = tmem + kColQ + lane_base + (uint32_t)(cq * kQCols);
+      if constexpr (kQCols == 16) tmem_st16(ta, qv);
+      else tmem_st8(ta, qv);
+      tmem_wait_st();
+      tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar(Q_FULL + x));
-      if (t == 0 && h == 0) TC_TRACE(2 + x, 4, g);
+      if (lane == 0) mbar_arrive(bar(Q_FULL));
     };
-    bool q_pending = false;  // Q of the next x-live item issued, Q_FULL not yet arrived
-    {
-      const ItemSlot* s0 = wait_item(0);
-      if (s0->idx >= 0 && x_live(s0)) {
-        mbar_wait(bar(Q_EMPTY + x), (ni & 1) ^ 1);
-        issue_q(s0);
-        q_pending = true;
-      }
+
+    wait_item(0);
+    if (fld(0, kFIdx) >= 0) {
+      uint32_t qv[kQCols];
+      load_q(0, qv);
+      store_q(qv);  // the Q region is free at kernel start
     }
     for (uint32_t n = 0;; ++n) {
-      const ItemSlot* cs = ring + (n & 1);  // ITEM_FULL(n) already waited
-      if (cs->idx < 0) break;
-      const int ntok = cs->item.ntok;
+      if (fld(n, kFIdx) < 0) break;  // ITEM_FULL(n) already waited
+      const int ntok = fld(n, kFNtok);
       const int ntiles = (ntok + kN - 1) / kN;
-      if (!x_live(cs)) {
-        // tile B idle for this item; prefetch Q if the next item uses it
-        g += ntiles;
-        const ItemSlot* ns = wait_item(n + 1);
-        if (ns->idx >= 0 && x_live(ns)) {
-          mbar_wait(bar(Q_EMPTY + x), (ni & 1) ^ 1);
-          issue_q(ns);
-          q_pending = true;
-        }
-        release_item(n);
-        continue;
-      }
-      if (q_pending) {
-        finish_q();
-        q_pending = false;
-      }
-
       float m_ref = -INFINITY;  // running max, log2 units
       float2 l2 = make_float2(0.f, 0.f);
+      bool have_next = false;
+      uint32_t qn[kQCols];
       for (int j = 0; j < ntiles; ++j, ++c, ++g) {
-        mbar_wait(bar(S_FULL + x), c & 1);
-        if (t == 0 && h == 0) TC_TRACE(2 + x, 0, g);
+        const uint32_t b = c & 1;
+        mbar_wait(bar(S_FULL + b), (c >> 1) & 1);
+        if (tr) TC_TRACE(2, 0, g);
         tc_fence_after();
-        uint32_t sr[32];
-        tmem_ld32(tS(x) + lane_base + 32 * h, sr);
+        uint32_t sr[16];
+        tmem_ld16(tmem + kColS + 64u * b + lane_base + (uint32_t)(16 * cq), sr);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar(S_EMPTY + x));
+        if (lane == 0) mbar_arrive(bar(S_EMPTY + b));
+        if (tr) TC_TRACE(2, 6, g);
         if (j == ntiles - 1) {
-          // last KV tile: this item's last QK is done, so the Q tile is free --
-          // start copying the next item's Q rows now
-          const ItemSlot* ns = wait_item(n + 1);
-          if (ns->idx >= 0 && x_live(ns)) {
-            mbar_wait(bar(Q_EMPTY + x), ni & 1);
-            issue_q(ns);
-            q_pending = true;
-          }
+          // last KV tile: fetch the next item and start loading its Q rows
+          wait_item(n + 1);
+          have_next = fld(n + 1, kFIdx) >= 0;
+          if (have_next) load_q(n + 1, qn);
         }
 
-        const int valid = ntok - j * kN - 32 * h;  // valid columns of this half
-        if (valid < 32) {
+        const int valid = ntok - j * kN - 16 * cq;  // valid columns of this quarter
+        if (valid < 16) {
 #pragma unroll
-          for (int k = 0; k < 32; ++k)
+          for (int k = 0; k < 16; ++k)
             if (k >= valid) sr[k] = __float_as_uint(-INFINITY);
         }
-        float pm[11];
+        float pm[6];
 #pragma unroll
-        for (int k = 0; k < 10; ++k)
+        for (int k = 0; k < 5; ++k)
           pm[k] = fmax3(__uint_as_float(sr[3 * k]), __uint_as_float(sr[3 * k + 1]), __uint_as_float(sr[3 * k + 2]));
-        pm[10] = fmaxf(__uint_as_float(sr[30]), __uint_as_float(sr[31]));
-        float pmx = fmax3(fmax3(pm[0], pm[1], pm[2]), fmax3(pm[3], pm[4], pm[5]),
-                          fmax3(fmax3(pm[6], pm[7], pm[8]), pm[9], pm[10]));
-        *red_at(xc & 1, h) = pmx;
-        named_bar_sync(pair_bar, 64);
-        const float mx = fmaxf(pmx, *red_at(xc & 1, h ^ 1)) * scale_log2;
+        pm[5] = __uint_as_float(sr[15]);
+        const float pmx = fmax3(fmax3(pm[0], pm[1], pm[2]), pm[3], fmaxf(pm[4], pm[5]));
+        sts_f32(red_at(xc & 1, cq), pmx);
+        named_bar_sync(quarter_bar, 128);
+        const float mx = fmaxf(fmax3(lds_f32(red_at(xc & 1, 0)), lds_f32(red_at(xc & 1, 1)), lds_f32(red_at(xc & 1, 2))),
+                               lds_f32(red_at(xc & 1, 3))) *
+                         scale_log2;
         ++xc;
+        if (tr) TC_TRACE(2, 7, g);
         const bool need = mx > m_ref + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
           const float m_new = need ? mx : m_ref;
           const float alpha = ex2_approx(m_ref - m_new);
           if (j > 0) {
-            mbar_wait(bar(O_DONE + x), (c - 1) & 1);
+            // O must hold PV(c-1): wait for the PV that read P[(c-1)&1]
+            mbar_wait(bar(P_FREE + ((c - 1) & 1)), ((c - 1) >> 1) & 1);
             tc_fence_after();
 #pragma unroll
-            for (int q = 0; q < D / 32; ++q) {
+            for (int q = 0; q < kOCols / 16; ++q) {
               uint32_t o[16];
-              const uint32_t ta = tO(x) + lane_base + (uint32_t)(h * (D / 2) + q * 16);
+              const uint32_t ta = tmem + kColO + lane_base + (uint32_t)(cq * kOCols + q * 16);
               tmem_ld16(ta, o);
 #pragma unroll
               for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
@@ -542,49 +488,41 @@ __global__ void __launch_bounds__(kThreads, 1)
           l2.y *= alpha;
           m_ref = m_new;
         }
-        // P = exp2(s * scale - m_ref), packed 16-bit pairs (hi: 16 cols, lo: 16
-        // cols), computed and stored in two chunks of 16 columns
+        // P = exp2(s * scale - m_ref) for this quarter's 16 tokens, packed pairs
         const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_ref, -m_ref);
+        uint32_t ph[8], pl[8];
 #pragma unroll
-        for (int q2 = 0; q2 < 2; ++q2) {
-          uint32_t ph[8], pl[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int kk = q2 * 8 + k;
-            float2 a = __ffma2_rn(make_float2(__uint_as_float(sr[2 * kk]), __uint_as_float(sr[2 * kk + 1])), sc2, nm2);
-            a.x = ex2_approx(a.x);
-            a.y = ex2_approx(a.y);
-            ph[k] = Fmt<T>::pack(a.x, a.y);
-            if constexpr (kSplit) {
-              const float2 hf = make_float2(__uint_as_float(ph[k] << 16), __uint_as_float(ph[k] & 0xffff0000u));
-              const float2 lo = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
-              pl[k] = Fmt<T>::pack(lo.x, lo.y);
-              l2 = __fadd2_rn(l2, a);
-            } else {
-              // normalise by the sum of the ROUNDED weights the MMA actually uses:
-              // the output is then an exact weighted average of V rows
-              l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
-            }
+        for (int k = 0; k < 8; ++k) {
+          float2 a = __ffma2_rn(make_float2(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sc2, nm2);
+          a.x = ex2_approx(a.x);
+          a.y = ex2_approx(a.y);
+          ph[k] = Fmt<T>::pack(a.x, a.y);
+          if constexpr (kSplit) {
+            const float2 hf = Fmt<T>::unpack(ph[k]);
+            const float2 lo = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
+            pl[k] = Fmt<T>::pack(lo.x, lo.y);
+            l2 = __fadd2_rn(l2, a);
+          } else {
+            // normalise by the sum of the ROUNDED weights the MMA actually uses:
+            // the output is then an exact weighted average of V rows
+            l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
           }
-          if (q2 == 0) {
-            if (t == 0 && h == 0) TC_TRACE(2 + x, 1, g);
-            // the P columns are free once PV of the previous tile completed
-            if (j > 0) {
-              mbar_wait(bar(O_DONE + x), (c - 1) & 1);
-              tc_fence_after();
-            }
-            if (t == 0 && h == 0) TC_TRACE(2 + x, 2, g);
-          }
-          tmem_st8(tP(x) + lane_base + 16 * h + 8 * q2, ph);
-          if constexpr (kSplit) tmem_st8(tP(x) + lane_base + 32 + 16 * h + 8 * q2, pl);
         }
+        if (tr) TC_TRACE(2, 1, g);
+        // P[b] is free once the PV of tile c-2 completed
+        mbar_wait(bar(P_FREE + b), ((c >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (tr) TC_TRACE(2, 2, g);
+        const uint32_t tp = tmem + kColP + 64u * b + lane_base + (uint32_t)(8 * cq);
+        tmem_st8(tp, ph);
+        if constexpr (kSplit) tmem_st8(tp + 32, pl);
         if (j * kN + kN > ntok) {
-          // tail tile: zero V rows past the span (both tiles may do it: same zeros)
+          // tail tile: zero V rows past the span (stale / uninitialised smem)
           const int vt = ntok - j * kN;
           const int s = g % kStages;
           mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
           const int nz = (kN - vt) * L::KB * 8;
-          for (int q = h * kM + t; q < nz; q += 2 * kM) {
+          for (int q = cq * kM + t; q < nz; q += 4 * kM) {
             const int rr = vt + q / (L::KB * 8);
             const int kb = (q / 8) % L::KB, ch = q % 8;
             st_shared_v4(sV(s) + kb * (kN * 128) + rr * 128 + (ch << 4), make_uint4(0, 0, 0, 0));
@@ -594,32 +532,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar(P_FULL + x));
-        if (t == 0 && h == 0) TC_TRACE(2 + x, 3, g);
+        if (lane == 0) mbar_arrive(bar(P_FULL + b));
+        if (tr) TC_TRACE(2, 3, g);
       }
 
-      // the next item's first QK can now overlap this epilogue
-      if (q_pending) {
-        finish_q();
-        q_pending = false;
+      // next item's Q -> TMEM once this item's last QK completed, so its first
+      // QK overlaps this epilogue
+      if (have_next) {
+        mbar_wait(bar(Q_EMPTY), ni & 1);
+        tc_fence_after();
+        store_q(qn);
+        if (tr) TC_TRACE(2, 4, g);
       }
-      // epilogue: O / l; the halves exchange their partial l
-      float lh = l2.x + l2.y;
-      *red_at(xc & 1, h) = lh;
-      named_bar_sync(pair_bar, 64);
-      const float l = lh + *red_at(xc & 1, h ^ 1);
+      // epilogue: O / l; the 4 column quarters exchange their partial l
+      const float lh = l2.x + l2.y;
+      sts_f32(red_at(xc & 1, cq), lh);
+      named_bar_sync(quarter_bar, 128);
+      const float l = (lds_f32(red_at(xc & 1, 0)) + lds_f32(red_at(xc & 1, 1))) +
+                      (lds_f32(red_at(xc & 1, 2)) + lds_f32(red_at(xc & 1, 3)));
       ++xc;
-      const bool live = r < cs->item.nrows;
-      const int2 meta = live ? cs->meta[r] : make_int2(0, -1);
-      const int head = cs->item.kvh * G + (live ? (cs->item.row0 + r) % G : 0);
-      mbar_wait(bar(O_DONE + x), (c - 1) & 1);
+      const bool live = t < fld(n, kFNrows);
+      const int2 meta = live ? lds_v2(ring_s + (n & 1) * kSlotBytes + kFMeta + 8 * t) : make_int2(0, -1);
+      const int head = fld(n, kFKvh) * G + (live ? (fld(n, kFRow0) + t) % G : 0);
+      mbar_wait(bar(P_FREE + ((c - 1) & 1)), ((c - 1) >> 1) & 1);  // last PV done
       tc_fence_after();
       const float inv = 1.f / l;
 #pragma unroll
-      for (int q = 0; q < D / 32; ++q) {
+      for (int q = 0; q < kOCols / 16; ++q) {
         uint32_t o[16];
-        const int col = h * (D / 2) + q * 16;
-        tmem_ld16(tO(x) + lane_base + (uint32_t)col, o);
+        const int col = cq * kOCols + q * 16;
+        tmem_ld16(tmem + kColO + lane_base + (uint32_t)col, o);
         if (live) {
           if (meta.y < 0) {
             uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)meta.x * H + head) * D + col);
@@ -639,11 +581,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (live && meta.y >= 0 && h == 0) part_lse[(int64_t)meta.y * H + head] = m_ref + log2f(l);
+      if (live && meta.y >= 0 && cq == 0) part_lse[(int64_t)meta.y * H + head] = m_ref + log2f(l);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar(O_EMPTY + x));
-      if (t == 0 && h == 0) TC_TRACE(2 + x, 5, g - 1);
+      if (lane == 0) mbar_arrive(bar(O_EMPTY));
+      if (tr) TC_TRACE(2, 5, g - 1);
       release_item(n);
       ++ni;
     }

@@ -87,7 +87,8 @@ def main():
     names = {(0, 0): "prod_kvempty", (1, 5): "mma_item_qfull", (1, 0): "mma_kvfull", (1, 3): "qkA_start",
              (1, 1): "mma_qk_issued",
              (1, 4): "pvA_start(j-1)", (1, 2): "mma_pv_issued",
-             (2, 4): "smA_qstored", (2, 0): "smA_sfull", (2, 1): "smA_exp_done", (2, 2): "smA_odone",
+             (2, 4): "smA_qstored", (2, 0): "smA_sfull", (2, 6): "smA_sloaded", (2, 7): "smA_maxed",
+             (2, 1): "smA_exp_done", (2, 2): "smA_odone",
              (2, 3): "smA_pfull", (2, 5): "smA_epi_done",
              (3, 0): "smB_sfull", (3, 1): "smB_exp_done", (3, 2): "smB_odone", (3, 3): "smB_pfull"}
     hdr = " step " + " ".join(f"{v:>15s}" for v in names.values())
