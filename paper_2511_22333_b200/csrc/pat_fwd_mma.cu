@@ -21,6 +21,7 @@
 #include <cuda_fp16.h>
 
 #include "pat_plan.cuh"
+#include "pat_sm100.cuh"
 
 namespace pat {
 
@@ -218,9 +219,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     // One thread: item descriptors one item ahead, block ids one stage ahead
     // (independent loads, latency hidden behind the ring wait), Q rows by bulk
     // copy, K/V page slices by TMA.
-    if (lane != 0) return;
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmk) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmv) : "memory");
+    // Whole warp (warp-uniform TMA operands: lane i fetches page group i's
+    // block id, broadcast by shuffle); lane 0 issues.
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmk) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmv) : "memory");
+    }
     uint32_t g = 0, n = 0;
     int it = blockIdx.x;
     Item item;
@@ -232,13 +236,6 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       const int h = item.kvh, ntok = item.ntok;
       const int32_t* blist = plan.pack_blk + item.blk;
       const int nst = (ntok + kStageTok - 1) / kStageTok;
-      auto stage_ids = [&](int st, int* b4) {
-#pragma unroll
-        for (int gr = 0; gr < 4; ++gr) {
-          const int tok = st * kStageTok + gr * 16;
-          b4[gr] = tok < ntok ? __ldg(blist + tok / bs) : 0;
-        }
-      };
 #if !(defined(PAT_STREAM_NOCOMPUTE) && PAT_STREAM_NOCOMPUTE >= 2)
       {
         const uint32_t qb = n & 1;
@@ -246,8 +243,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         const int r_end = item.row0 + item.nrows;
         const int i0 = item.row0 / G, i1 = (r_end - 1) / G;
         mbar_wait(qempty0 + 8 * qb, ((n >> 1) & 1) ^ 1);
-        mbar_expect_tx(qfull0 + 8 * qb, (uint32_t)(item.nrows * D * 2));
-        for (int i = i0; i <= i1; ++i) {
+        if (lane == 0) mbar_expect_tx(qfull0 + 8 * qb, (uint32_t)(item.nrows * D * 2));
+        __syncwarp();
+        for (int i = i0 + lane; i <= i1; i += 32) {
           const int a = max(i * G, item.row0), e = min((i + 1) * G, r_end);
           const int qid = __ldg(plan.pack_q + item.qoff + i);
           const T* src = qg + ((int64_t)qid * H + h * G + (a - i * G)) * D;
@@ -260,30 +258,28 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         const int rem = ntok - st * kStageTok;
         const int ngrp = rem >= kStageTok ? kStageTok / 16 : (rem + 15) / 16;
         const uint32_t dk = sbase + s * S::kStageBytes, dv = dk + S::kTileBytes;
-        mbar_wait(empty0 + 8 * s, ((g / NS) & 1) ^ 1);
-        mbar_expect_tx(full0 + 8 * s, (uint32_t)(ngrp * S::KB * 2048 * 2));
-#ifdef PAT_PRODUCER_BURST
-        int b4[4];
-        stage_ids(st, b4);
-#endif
-        for (int gr = 0; gr < ngrp; ++gr) {
-          const int tok = st * kStageTok + gr * 16;
-          // Dependent id load per page slice: the load latency paces the TMA
-          // issue, which measured faster than issuing a stage's 16 boxes as a
-          // burst (tools/kv_stream_probe.cu, profiles/).
-#ifdef PAT_PRODUCER_BURST
-          const int blk = b4[gr];
-#else
+        int my_blk = 0, my_off = 0;
+        if (lane < ngrp) {
+          const int tok = st * kStageTok + lane * 16;
           const int pg = bs == 16 ? (tok >> 4) : tok / bs;
-          const int blk = __ldg(blist + pg);
-#endif
-          const int off = bs == 16 ? 0 : tok - pg * bs;
+          my_blk = __ldg(blist + pg);
+          my_off = bs == 16 ? 0 : tok - pg * bs;
+        }
+        mbar_wait(empty0 + 8 * s, ((g / NS) & 1) ^ 1);
+        if (lane == 0) mbar_expect_tx(full0 + 8 * s, (uint32_t)(ngrp * S::KB * 2048 * 2));
+        __syncwarp();
+        for (int gr = 0; gr < ngrp; ++gr) {
+          const int blk = __shfl_sync(0xffffffffu, my_blk, gr);
+          const int off = __shfl_sync(0xffffffffu, my_off, gr);
+          if (sm100::elect_one()) {
 #pragma unroll
-          for (int kb = 0; kb < S::KB; ++kb) {
-            const uint32_t o = (uint32_t)((gr * S::KB + kb) * 2048);
-            tma_load_4d(dk + o, &tmk, full0 + 8 * s, kb * 64, h, off, blk);
-            tma_load_4d(dv + o, &tmv, full0 + 8 * s, kb * 64, h, off, blk);
+            for (int kb = 0; kb < S::KB; ++kb) {
+              const uint32_t o = (uint32_t)((gr * S::KB + kb) * 2048);
+              tma_load_4d(dk + o, &tmk, full0 + 8 * s, kb * 64, h, off, blk);
+              tma_load_4d(dv + o, &tmv, full0 + 8 * s, kb * 64, h, off, blk);
+            }
           }
+          __syncwarp();
         }
       }
       item = next_item;

@@ -90,7 +90,7 @@ def main():
              (2, 4): "smA_qstored", (2, 0): "smA_sfull", (2, 6): "smA_sloaded", (2, 7): "smA_maxed",
              (2, 1): "smA_exp_done", (2, 2): "smA_odone",
              (2, 3): "smA_pfull", (2, 5): "smA_epi_done",
-             (3, 0): "smB_sfull", (3, 1): "smB_exp_done", (3, 2): "smB_odone", (3, 3): "smB_pfull"}
+             (3, 0): "sm_nextitem", (3, 1): "sm_qloads_issued", (3, 2): "sm_qempty"}
     hdr = " step " + " ".join(f"{v:>15s}" for v in names.values())
     print(hdr)
     n = min(args.steps, ntok // 64) if ntok else args.steps
@@ -108,5 +108,30 @@ def main():
         print(f"steady-state cycles/step (mma kvfull): median {np.median(d):.0f} mean {d.mean():.0f}")
 
 
+def analyse(path):
+    """Per-step breakdown of a saved trace log (softmax busy / idle, MMA KV waits)."""
+    lines = open(path).read().splitlines()
+    hdr = lines[1].split()
+    rows = [dict(zip(hdr, map(int, l.split()))) for l in lines[2:] if l.split() and l.split()[0].isdigit()]
+    prev = None
+    tot = {"sm_busy": 0, "sm_wait_s": 0, "mma_kv_wait": 0}
+    for r in rows:
+        if r["smA_sfull"] <= 0:
+            break
+        busy = r["smA_pfull"] - r["smA_sfull"]
+        wait = r["smA_sfull"] - prev["smA_pfull"] if prev else 0
+        kvw = r["mma_kvfull"] - max(prev["mma_pv_issued"], prev["mma_qk_issued"]) if prev else 0
+        item = " <item" if r.get("mma_item_qfull", -1) > 0 else ""
+        print(f"{r['step']:4d} sm_busy {busy:6d} sm_wait_S {wait:6d} mma_kv_wait {kvw:6d}{item}")
+        tot["sm_busy"] += busy
+        tot["sm_wait_s"] += wait
+        tot["mma_kv_wait"] += max(kvw, 0)
+        prev = r
+    print(tot)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) == 3 and sys.argv[1] == "--analyse":
+        analyse(sys.argv[2])
+    else:
+        main()
