@@ -72,8 +72,9 @@ typedef struct pat_plan_options {
   int32_t num_sms;      /* 0 = query the current device */
   int32_t flags;        /* pat_plan_flags */
   int32_t tc_min_rows;  /* packs with >= this many rows (queries x G) use the tcgen05 kernel,
-                           the others the mma.sync streaming kernel; 0 = default (1: every
-                           pack on the tcgen05 kernel), < 0 = never */
+                           the others the mma.sync streaming kernel; 0 = library default
+                           (every pack on the tcgen05 kernel, unless no pack has more than
+                           16 rows: then all on the streaming kernel), < 0 = never */
 } pat_plan_options;
 
 typedef struct pat_plan_info {

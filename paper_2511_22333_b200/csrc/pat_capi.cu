@@ -52,6 +52,7 @@ using namespace pat;
 
 struct pat_plan {
   int B = 0, bs = 16, H = 0, KVH = 0, d = 0, split_mode = 0, num_sms = 148, tc_min_rows = 64;
+  bool tc_auto = false;  // tc_min_rows left to the library (options value 0)
   bool on_device = false;
   HostPacks packs;
   HostSchedule sched;
@@ -102,6 +103,7 @@ void init_plan(pat_plan* P, int B, int bs, const pat_plan_options* opt) {
   P->d = opt->head_dim;
   P->split_mode = opt->split_mode;
   P->num_sms = opt->num_sms;
+  P->tc_auto = opt->tc_min_rows == 0;
   P->tc_min_rows = opt->tc_min_rows == 0 ? 1 : (opt->tc_min_rows < 0 ? 0 : opt->tc_min_rows);
   if (P->d != 64 && P->d != 128) P->tc_min_rows = 0;
   if (P->num_sms <= 0) {
@@ -179,6 +181,17 @@ int upload(pat_plan* P) {
 }
 
 int finish_plan(pat_plan* P, const RowsView& R, int flags) {
+  if (P->tc_auto) {
+    // Kernel choice: every pack goes to the tcgen05 kernel (one persistent
+    // kernel, dynamic load balance), except when no pack is wider than one
+    // 16-row mma.sync tile (e.g. a batch without prefix sharing): then the
+    // HBM-paced streaming kernel alone is faster (measured: c5 694 vs 800 us).
+    int max_rows = 0;
+    const int G = P->H / P->KVH;
+    for (int p = 0; p < P->packs.n_packs(); ++p)
+      max_rows = std::max(max_rows, (P->packs.q_off[p + 1] - P->packs.q_off[p]) * G);
+    P->tc_min_rows = max_rows <= 16 ? 0 : 1;
+  }
   ScheduleParams sp{P->B, P->bs, P->H, P->KVH, P->d, P->split_mode, P->num_sms, P->tc_min_rows};
   int st = host_schedule(P->packs, sp, &P->sched);
   if (st) return st;
