@@ -278,7 +278,7 @@ class _Null:
 
 
 def _launches(plan):
-    """Kernels per layer: one forward kernel per non-empty variant + the merge."""
+    """Kernels per layer: the forward kernel(s) + the merge (when partials exist)."""
     return plan.info().n_launches
 
 
@@ -418,7 +418,9 @@ def main():
                          "frac": round(gbs / peaks["hbm_gbs"], 4),
                          "traffic": traffic["bytes"] if traffic else None,
                          "traffic_source": traffic["source"] if traffic else None,
-                         "kernel": "one decode-attention layer (CUDA graph: forward kernels on their SM shares + merge); traffic = sum of its kernels (ncu)",
+                         "kernel": "one decode-attention layer replayed as a CUDA graph: the forward kernel (tcgen05 "
+                                   "fwd_tc2_kernel; fwd_stream_kernel for all-narrow plans) + merge_kernel; achieved = "
+                                   "unique KV bytes / layer time; traffic = DRAM read+write of the layer's kernels (ncu)",
                          "peak_source": peaks["source"]},
             "e2e": {"value": round(tot_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": main_res["e2e"]["h2d"], "d2h_bytes_per_step": main_res["e2e"]["d2h"],
