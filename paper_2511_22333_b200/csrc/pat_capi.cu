@@ -146,6 +146,9 @@ int upload(pat_plan* P) {
   }
   size_t o_nit = b.add(nit, sizeof(nit));
   size_t o_mq = b.addv(s.merge_q), o_qso = b.addv(s.q_slot_off), o_qn = b.addv(s.q_nslot);
+  std::vector<int32_t> mdesc;
+  for (int32_t q : s.merge_q) mdesc.insert(mdesc.end(), {q, s.q_slot_off[q], s.q_nslot[q], 0});
+  size_t o_md = b.addv(mdesc);
   int32_t nm = (int32_t)s.merge_q.size();
   size_t o_nm = b.add(&nm, sizeof(nm));
   const int32_t zeros[16] = {};
@@ -167,6 +170,7 @@ int upload(pat_plan* P) {
   for (int v = 0; v < NUM_VARIANTS; ++v) D.items[v] = (const Item*)(base + o_it[v]);
   D.n_items = (const int32_t*)(base + o_nit);
   D.merge_q = (const int32_t*)(base + o_mq);
+  D.merge_desc = (const int4*)(base + o_md);
   D.q_slot_off = (const int32_t*)(base + o_qso);
   D.q_nslot = (const int32_t*)(base + o_qn);
   D.n_merge = (const int32_t*)(base + o_nm);

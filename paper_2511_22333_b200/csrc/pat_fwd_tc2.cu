@@ -234,12 +234,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t n = 0;; ++n) {
       const uint32_t slot = n & 1;
       mbar_wait(bar(ITEM_EMPTY + slot), ((n >> 1) & 1) ^ 1);
-      int it = 0;
-      if (lane == 0) {
-        it = atomicAdd(plan.sched, 1);
-        if (it >= n_items) it = -1;
-      }
+      // the first item of CTA b is item b (no claim latency at kernel start),
+      // later ones come from the counter, offset by the grid
+      int it = (int)blockIdx.x;
+      if (n > 0 && lane == 0) it = atomicAdd(plan.sched, 1) + (int)gridDim.x;
       it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= n_items) it = -1;
       Item item{};
       if (it >= 0) {
         item = load_item(items + it);

@@ -38,8 +38,52 @@ __device__ __forceinline__ void merge_rows(const DevPlan& plan, const float* __r
   const int lane = threadIdx.x & 31;
   constexpr int PER = D / 32;
   for (int w = gw; w < nq * H; w += nw) {
-    const int q = __ldg(plan.merge_q + w / H), head = w % H;
-    const int base = __ldg(plan.q_slot_off + q), n = __ldg(plan.q_nslot + q);
+    const int4 md = __ldg(plan.merge_desc + w / H);
+    const int q = md.x, head = w % H, base = md.y, n = md.z;
+    if (n <= 8) {
+      // common case: every slot's LSE and O row are loaded at once (one round
+      // trip after the descriptor), then folded
+      const float lse = lane < n ? __ldcg(part_lse + (int64_t)(base + lane) * H + head) : -INFINITY;
+      float v[8][PER];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (u < n) {
+          const float* src = part_o + ((int64_t)(base + u) * H + head) * D + lane * PER;
+          if constexpr (PER == 4) {
+            const float4 x = __ldcg(reinterpret_cast<const float4*>(src));
+            v[u][0] = x.x, v[u][1] = x.y, v[u][2] = x.z, v[u][3] = x.w;
+          } else {
+            const float2 x = __ldcg(reinterpret_cast<const float2*>(src));
+            v[u][0] = x.x, v[u][1] = x.y;
+          }
+        }
+      }
+      float M = lse;
+#pragma unroll
+      for (int off = 4; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      M = __shfl_sync(0xffffffffu, M, 0);
+      const float f = lane < n ? exp2f(lse - M) : 0.f;
+      float L = f;
+#pragma unroll
+      for (int off = 4; off; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+      L = __shfl_sync(0xffffffffu, L, 0);
+      float acc[PER];
+#pragma unroll
+      for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float fu = __shfl_sync(0xffffffffu, f, u);
+        if (u < n)
+#pragma unroll
+          for (int e = 0; e < PER; ++e) acc[e] += fu * v[u][e];
+      }
+      const float inv = 1.f / L;
+      T* dst = out + ((int64_t)q * H + head) * D + lane * PER;
+#pragma unroll
+      for (int e = 0; e < PER; e += 2)
+        *reinterpret_cast<uint32_t*>(dst + e) = MergeOut<T>::pack(acc[e] * inv, acc[e + 1] * inv);
+      continue;
+    }
     float acc[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) acc[e] = 0.f;

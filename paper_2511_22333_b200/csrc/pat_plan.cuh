@@ -52,6 +52,7 @@ struct DevPlan {
   const Item* items[NUM_VARIANTS];
   const int32_t* n_items;       // [NUM_VARIANTS] (device counts)
   const int32_t* merge_q;       // [n_merge_q] queries with > 1 unit
+  const int4* merge_desc;       // [n_merge_q] (query, first slot, slots, 0): one load per merge row
   const int32_t* q_slot_off;    // [B] first slot of the query
   const int32_t* q_nslot;       // [B] slots of the query (0 or >= 2)
   const int32_t* n_merge;       // [1]
