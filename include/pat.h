@@ -105,6 +105,13 @@ int pat_plan_create_device(int32_t B, const int32_t* block_tables, int64_t bt_st
                            const int32_t* seq_lens, int32_t max_blocks, int32_t block_size,
                            const pat_plan_options* opt, void* stream, pat_plan** out);
 
+/* Device table fingerprint for the lazy plan update (PackCache, packer.py:189-221):
+ * 64-bit hash of (B, block_size, seq_lens, the used block ids of every row) written
+ * to out_hash (device-accessible).  Stream-ordered; one small kernel. */
+int pat_table_hash_device(int32_t B, const int32_t* block_tables, int64_t bt_stride,
+                          const int32_t* seq_lens, int32_t block_size, uint64_t* out_hash,
+                          void* stream);
+
 /* Explicit partition: unit u has queries unit_q[unit_q_off[u] .. unit_q_off[u+1]),
  * blocks unit_blk[unit_blk_off[u] .. unit_blk_off[u+1]) and unit_kv[u] tokens.
  * Coverage against the table is checked (PAT_ERR_COVERAGE_GAP). */

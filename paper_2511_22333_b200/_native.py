@@ -40,6 +40,8 @@ class PlanInfo(C.Structure):
 SIGNATURES = [
     ("pat_plan_create_host", C.c_int, [C.c_int32, i64p, i32p, i32p, C.c_int32, C.POINTER(PlanOptions),
                                        C.POINTER(C.c_void_p)]),
+    ("pat_table_hash_device", C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p,
+                                        C.c_void_p]),
     ("pat_plan_create_device", C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32,
                                          C.POINTER(PlanOptions), C.c_void_p, C.POINTER(C.c_void_p)]),
     ("pat_plan_create_units", C.c_int, [C.c_int32, i64p, i32p, i32p, C.c_int32, C.c_int32, i64p, i32p, i64p,

@@ -100,6 +100,44 @@ class PatDecoder:
         plan = self.plan_for(table)
         return pat_attention(plan, q, k_cache, v_cache, out=out, workspace=self.workspace(plan), scale=scale)
 
+    # -- device block tables (vLLM layout) ---------------------------------------------
+    def table_hash(self, block_tables, seq_lens, block_size: int = 16, stream=None) -> int:
+        """Device fingerprint of (block_tables [B, max_blocks], seq_lens [B]) int32 CUDA
+        tensors (``pat_table_hash_device``), read back through pinned memory (one
+        event wait -- the only host sync of the device lazy-update path)."""
+        bt = block_tables.contiguous()
+        sl = seq_lens.contiguous()
+        s = stream if stream is not None else torch.cuda.current_stream(bt.device)
+        if getattr(self, "_hash_dev", None) is None or self._hash_dev.device != bt.device:
+            self._hash_dev = torch.empty(1, dtype=torch.int64, device=bt.device)
+            self._hash_host = torch.empty(1, dtype=torch.int64).pin_memory()
+        N.check(N.lib().pat_table_hash_device(bt.shape[0], C.c_void_p(bt.data_ptr()), bt.stride(0),
+                                              C.c_void_p(sl.data_ptr()), block_size,
+                                              C.c_void_p(self._hash_dev.data_ptr()), C.c_void_p(s.cuda_stream)),
+                "pat_table_hash_device")
+        with torch.cuda.stream(s):
+            self._hash_host.copy_(self._hash_dev, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        ev.synchronize()
+        return int(self._hash_host.item()) & 0xFFFFFFFFFFFFFFFF
+
+    def plan_for_device(self, block_tables, seq_lens, block_size: int = 16) -> PatPlan:
+        """Lazy update for device tables: reuse the plan while the device fingerprint
+        is unchanged, else re-plan with the GPU packer (``pat_plan_create_device``)."""
+        key = f"dev:{self.table_hash(block_tables, seq_lens, block_size):016x}"
+        plan = self.cache.lookup(key)
+        if plan is None:
+            plan = PatPlan.from_device_table(block_tables, seq_lens, block_size, self.num_heads, self.num_kv_heads,
+                                             self.head_dim, split=self.split, tc_min_rows=self.tc_min_rows)
+            self.cache.store(key, plan)
+        return plan
+
+    def forward_device(self, block_tables, seq_lens, q, k_cache, v_cache, out=None, scale=None):
+        """Decode attention straight from vLLM-style device block tables."""
+        plan = self.plan_for_device(block_tables, seq_lens, k_cache.shape[1])
+        return pat_attention(plan, q, k_cache, v_cache, out=out, workspace=self.workspace(plan), scale=scale)
+
 
 class PatLayerGraph:
     """One decode-attention layer captured as a CUDA graph (the multi-stream

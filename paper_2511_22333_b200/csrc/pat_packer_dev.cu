@@ -15,6 +15,7 @@
 //   K9 members   : queries inside a pack in pi order, produces_partial
 // Output (device): packs as (rep query, first block, end block, kv_len,
 // query list, partial) in reference order; bit-exact with pack_batch.
+#include <algorithm>
 #include <cstdio>
 #include <vector>
 
@@ -551,4 +552,60 @@ int device_pack(const int32_t* d_bt, int64_t stride, const int32_t* d_seq, int B
   return PAT_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// Device table hash for the lazy update (PackCache keyed by a device fingerprint,
+// packer.py:189-221): 64-bit, order-sensitive over rows and positions, computed as
+// a sum of splitmix64-mixed terms so the reduction order does not matter.
+// ------------------------------------------------------------------------------------------
+namespace {
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// one warp per row: (row, position, block id) terms and (row, seq_len)
+__global__ void k_table_hash(const int32_t* __restrict__ bt, int64_t stride, const int32_t* __restrict__ seq, int B,
+                             int bs, unsigned long long* out) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  uint64_t acc = 0;
+  for (int q = w; q < B; q += nw) {
+    const int len = __ldg(seq + q);
+    const int nb = len > 0 ? (len + bs - 1) / bs : 0;
+    const uint64_t rowk = mix64(((uint64_t)q << 32) ^ 0xA5A5A5A5ull);
+    for (int j = lane; j < nb; j += 32)
+      acc += mix64(rowk ^ ((uint64_t)j << 32) ^ (uint32_t)__ldg(bt + (int64_t)q * stride + j));
+    if (lane == 0) acc += mix64(rowk + 0x5151ull + (uint64_t)(uint32_t)len);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+}  // namespace
+
 }  // namespace pat
+
+extern "C" int pat_table_hash_device(int32_t B, const int32_t* block_tables, int64_t bt_stride,
+                                     const int32_t* seq_lens, int32_t block_size, uint64_t* out_hash,
+                                     void* stream) {
+  if (!out_hash || B < 0 || block_size <= 0 || (B > 0 && (!block_tables || !seq_lens))) {
+    pat::set_error("bad arguments to pat_table_hash_device");
+    return PAT_ERR_SHAPE_MISMATCH;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // seed with (B, block_size) so the empty table and different page sizes differ
+  const uint64_t seed = ((uint64_t)(uint32_t)B << 32) ^ (uint64_t)(uint32_t)block_size ^ 0x7A7A000000000000ull;
+  cudaError_t e = cudaMemcpyAsync(out_hash, &seed, sizeof(seed), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && B > 0) {
+    const int blocks = std::min(148 * 4, (B + 7) / 8);
+    pat::k_table_hash<<<blocks, 256, 0, st>>>(block_tables, bt_stride, seq_lens, B, block_size,
+                                             (unsigned long long*)out_hash);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    pat::set_error("pat_table_hash_device: %s", cudaGetErrorString(e));
+    return PAT_ERR_CUDA;
+  }
+  return PAT_OK;
+}

@@ -71,3 +71,41 @@ def test_device_plan_forward_matches_host_plan():
     assert pd.pack_tuples() == ph.pack_tuples()
     assert torch.equal(P.pat_attention(pd, q, kc, vc), P.pat_attention(ph, q, kc, vc))
     assert np.isfinite(1.0)
+
+
+def test_device_lazy_update():
+    """PatDecoder.forward_device: the device fingerprint (pat_table_hash_device)
+    reuses the plan for an unchanged table, re-plans (GPU packer) when a block id
+    or a length changes, and matches the host-table path bit for bit."""
+    w = configs.workload("c2")
+    table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    bt_np, sl_np = table.padded(max(len(r) for r in w.rows) + 3)
+    bt = torch.from_numpy(bt_np).cuda()
+    sl = torch.from_numpy(sl_np).cuda()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    nb = w.num_pool_blocks() + 1
+    kc = torch.randn(nb, 16, 8, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    vc = torch.randn(nb, 16, 8, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    q = torch.randn(w.batch, 32, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    dec = P.PatDecoder(32, 8, 128)
+    h0 = dec.table_hash(bt, sl)
+    assert dec.table_hash(bt.clone(), sl.clone()) == h0
+    out_dev = dec.forward_device(bt, sl, q, kc, vc).clone()
+    out_dev2 = dec.forward_device(bt, sl, q, kc, vc)
+    assert dec.cache.hits == 1 and dec.cache.misses == 1
+    out_host = dec(table, q, kc, vc)
+    torch.cuda.synchronize()
+    assert torch.equal(out_dev, out_dev2) and torch.equal(out_dev, out_host)
+    # padding past a row's length does not change the fingerprint ...
+    bt_pad = bt.clone()
+    bt_pad[0, -1] = 12345
+    assert dec.table_hash(bt_pad, sl) == h0
+    # ... a used block id or a length does
+    bt2 = bt.clone()
+    bt2[5, 0] = nb - 1
+    assert dec.table_hash(bt2, sl) != h0
+    sl2 = sl.clone()
+    sl2[7] -= 1
+    assert dec.table_hash(bt, sl2) != h0
+    dec.forward_device(bt, sl2, q, kc, vc)
+    assert dec.cache.misses == 3  # host-table call + the changed table
