@@ -109,3 +109,21 @@ def test_device_lazy_update():
     assert dec.table_hash(bt, sl2) != h0
     dec.forward_device(bt, sl2, q, kc, vc)
     assert dec.cache.misses == 3  # host-table call + the changed table
+
+
+def test_torch_op_decode_attention():
+    """torch.ops.patb200.decode_attention (vLLM-style tensors) == pat_attention."""
+    w = configs.workload("c1")
+    table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    bt_np, sl_np = table.padded()
+    g = torch.Generator(device="cuda").manual_seed(9)
+    nb = w.num_pool_blocks()
+    kv = torch.randn(2, nb, 16, 8, 128, device="cuda", dtype=torch.float16, generator=g)
+    q = torch.randn(w.batch, 32, 128, device="cuda", dtype=torch.float16, generator=g)
+    out = torch.empty_like(q)
+    torch.ops.patb200.decode_attention(q, kv[0], kv[1], torch.from_numpy(bt_np).cuda(),
+                                       torch.from_numpy(sl_np).cuda(), out, 0.0)
+    plan = PatPlan.from_table(table, 32, 8, 128)
+    ref = P.pat_attention(plan, q, kv[0].contiguous(), kv[1].contiguous())
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)

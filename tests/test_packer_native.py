@@ -173,3 +173,9 @@ def test_split_long_kv_python_api_matches_reference_fixture():
         assert got == as_split(c["split"]), c["name"]
     assert ctypes  # keep import
     assert np
+
+
+def test_torch_op_registered():
+    import torch
+    import paper_2511_22333_b200  # noqa: F401
+    assert hasattr(torch.ops.patb200, "decode_attention")
