@@ -36,13 +36,14 @@ void split_pack(int npages, int kv, int bs, int parts, std::vector<Part>& out) {
 
 // Estimated time (ns) of one work item of variant v with `rows` rows over
 // `ntok` tokens, measured on B200 (tools/tc_trace.py): the tcgen05 kernel runs
-// a 64-token KV tile of up to 128 rows in ~0.45 us (softmax / tensor bound;
-// one SM's HBM share is 32 KB per ~0.7 us when all SMs stream); the mma.sync
-// streaming kernel is HBM-paced.  Fixed cost: pipeline fill and the epilogue.
+// a 64-token KV tile of up to 128 rows in ~0.7 us (softmax-chain bound, about
+// one SM's HBM share of 32 KB when all SMs stream) plus ~3 us per item (next
+// item's KV and Q latency, epilogue); the mma.sync streaming kernel is
+// HBM-paced.
 double item_ns(const ScheduleParams& sp, int v, int rows, int ntok) {
   const double steps = (double)ceil_div(ntok, 64);
   const double dscale = sp.d / 128.0;
-  if (v == VAR_TC) return 1000.0 + steps * 450.0 * (0.5 + 0.5 * dscale);
+  if (v == VAR_TC) return 3000.0 + steps * 700.0 * (0.5 + 0.5 * dscale);
   const double bw = 6.0e3;  // bytes per ns (HBM, sustained)
   return 1500.0 + steps * 64.0 * sp.d * 4 / (bw / std::max(sp.num_sms, 1));
 }
