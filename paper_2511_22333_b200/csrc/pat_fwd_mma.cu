@@ -116,9 +116,10 @@ struct StreamSmem {
   static constexpr int kTileBytes = kStageTok * D * 2;  // one K or V stage tile
   static constexpr int kStageBytes = 2 * kTileBytes;
   // K+V ring: as deep as the 227 KB budget allows next to Q (x2) and the scratch
-  static constexpr int kNumStages = D == 128 ? (WM == 4 ? 4 : 5) : 8;
+  static constexpr int kNumStages = D == 128 ? (WM == 4 ? 4 : (WM == 2 ? 5 : 6)) : 8;
   static constexpr int kQBytes = WM * 16 * D * 2;       // linear [rows][D] (bulk-copied)
-  static constexpr int kScratchBytes = 4 * 16 * D * 4 + 2 * 4 * 16 * 4;  // epilogue: per-warp O, m, l
+  // epilogue: per-warp O for half of head_dim at a time (two passes), m, l
+  static constexpr int kScratchBytes = 4 * 16 * (D / 2) * 4 + 2 * 4 * 16 * 4;
   static constexpr int kOffQ = kNumStages * kStageBytes;  // two Q buffers
   static constexpr int kOffScratch = kOffQ + 2 * kQBytes;
   static constexpr int kOffBar = kOffScratch + kScratchBytes;
@@ -463,62 +464,63 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     }
     int next_qid = 0, next_slot = -1;
     if (nxt < n_items) load_meta(next_item, next_qid, next_slot);  // overlaps the epilogue
-    float* so = reinterpret_cast<float*>(smem + S::kOffScratch);  // [4 warps][16][D]
-    float* sm = so + 4 * 16 * D;                                  // [4][16]
+    constexpr int DH = D / 2;  // head-dim columns combined per pass
+    float* so = reinterpret_cast<float*>(smem + S::kOffScratch);  // [4 warps][16][D / 2]
+    float* sm = so + 4 * 16 * DH;                                 // [4][16]
     float* sl = sm + 4 * 16;                                      // [4][16]
-    named_sync(1, 128);  // previous item's scratch reads are done
-    {
-      const int ra = lane >> 2, rb = ra + 8, cb = 2 * (lane & 3);
-      float* wo = so + warp * 16 * D;
 #pragma unroll
-      for (int i = 0; i < D / 8; ++i) {
-        *reinterpret_cast<float2*>(wo + ra * D + i * 8 + cb) = make_float2(o[i][0], o[i][1]);
-        *reinterpret_cast<float2*>(wo + rb * D + i * 8 + cb) = make_float2(o[i][2], o[i][3]);
+    for (int pass = 0; pass < 2; ++pass) {
+      named_sync(1, 128);  // previous scratch reads are done
+      {
+        const int ra = lane >> 2, rb = ra + 8, cb = 2 * (lane & 3);
+        float* wo = so + warp * 16 * DH;
+#pragma unroll
+        for (int i = 0; i < D / 16; ++i) {
+          const int ii = pass * (D / 16) + i;
+          *reinterpret_cast<float2*>(wo + ra * DH + i * 8 + cb) = make_float2(o[ii][0], o[ii][1]);
+          *reinterpret_cast<float2*>(wo + rb * DH + i * 8 + cb) = make_float2(o[ii][2], o[ii][3]);
+        }
+        if (pass == 0 && (lane & 3) == 0) {
+          sm[warp * 16 + ra] = mrow[0];
+          sm[warp * 16 + rb] = mrow[1];
+          sl[warp * 16 + ra] = lrow[0];
+          sl[warp * 16 + rb] = lrow[1];
+        }
       }
-      if ((lane & 3) == 0) {
-        sm[warp * 16 + ra] = mrow[0];
-        sm[warp * 16 + rb] = mrow[1];
-        sl[warp * 16 + ra] = lrow[0];
-        sl[warp * 16 + rb] = lrow[1];
-      }
-    }
-    named_sync(1, 128);
+      named_sync(1, 128);
 #pragma unroll
-    for (int k = 0; k < ROWS / 4; ++k) {
-      const int r = warp + 4 * k;
-      const int qid = __shfl_sync(0xffffffffu, meta_qid, k);
-      const int slot = __shfl_sync(0xffffffffu, meta_slot, k);
-      if (r >= item.nrows || lane * 4 >= D) continue;
-      const int x = lane * 4;
-      const int tile = r / 16, rr = r % 16;
-      float M = -INFINITY;
+      for (int k = 0; k < ROWS / 4; ++k) {
+        const int r = warp + 4 * k;
+        const int qid = __shfl_sync(0xffffffffu, meta_qid, k);
+        const int slot = __shfl_sync(0xffffffffu, meta_slot, k);
+        if (r >= item.nrows || lane * 2 >= DH) continue;
+        const int x = lane * 2;  // within the pass's half
+        const int tile = r / 16, rr = r % 16;
+        float M = -INFINITY;
 #pragma unroll
-      for (int w = 0; w < WN; ++w) M = fmaxf(M, sm[(tile * WN + w) * 16 + rr]);
-      float L = 0.f;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int w = 0; w < WN; ++w) M = fmaxf(M, sm[(tile * WN + w) * 16 + rr]);
+        float L = 0.f;
+        float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int w = 0; w < WN; ++w) {
-        const int ww = tile * WN + w;
-        const float f = exp2f(sm[ww * 16 + rr] - M);
-        L += sl[ww * 16 + rr] * f;
-        const float4 v = *reinterpret_cast<const float4*>(so + (ww * 16 + rr) * D + x);
-        acc.x += v.x * f;
-        acc.y += v.y * f;
-        acc.z += v.z * f;
-        acc.w += v.w * f;
-      }
-      const float inv = 1.f / L;
-      const int head = h * G + (item.row0 + r) % G;
-      if (slot < 0) {
-        T* dst = out + ((int64_t)qid * H + head) * D + x;
-        uint2 pk;
-        pk.x = Vec2<T>::pack(acc.x * inv, acc.y * inv);
-        pk.y = Vec2<T>::pack(acc.z * inv, acc.w * inv);
-        *reinterpret_cast<uint2*>(dst) = pk;
-      } else {
-        float* dst = part_o + ((int64_t)slot * H + head) * D + x;
-        *reinterpret_cast<float4*>(dst) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-        if (lane == 0) part_lse[(int64_t)slot * H + head] = M + log2f(L);
+        for (int w = 0; w < WN; ++w) {
+          const int ww = tile * WN + w;
+          const float f = exp2f(sm[ww * 16 + rr] - M);
+          L += sl[ww * 16 + rr] * f;
+          const float2 v = *reinterpret_cast<const float2*>(so + (ww * 16 + rr) * DH + x);
+          acc.x += v.x * f;
+          acc.y += v.y * f;
+        }
+        const float inv = 1.f / L;
+        const int head = h * G + (item.row0 + r) % G;
+        const int xd = pass * DH + x;
+        if (slot < 0) {
+          T* dst = out + ((int64_t)qid * H + head) * D + xd;
+          *reinterpret_cast<uint32_t*>(dst) = Vec2<T>::pack(acc.x * inv, acc.y * inv);
+        } else {
+          float* dst = part_o + ((int64_t)slot * H + head) * D + xd;
+          *reinterpret_cast<float2*>(dst) = make_float2(acc.x * inv, acc.y * inv);
+          if (pass == 0 && lane == 0) part_lse[(int64_t)slot * H + head] = M + log2f(L);
+        }
       }
     }
     item = next_item;
