@@ -44,7 +44,10 @@ def load_traffic(config):
         return None
     with open(files[-1]) as fh:
         d = json.load(fh)
-    return {"bytes": int(d["layer_dram_bytes"]), "source": os.path.relpath(files[-1], REPO)}
+    per = d.get("per_kernel_dram_bytes", {})
+    fwd = [v for k, v in per.items() if "fwd_" in k]
+    return {"bytes": int(sum(fwd)) if fwd else int(d["layer_dram_bytes"]), "layer_bytes": int(d["layer_dram_bytes"]),
+            "source": os.path.relpath(files[-1], REPO)}
 
 
 def load_peaks():
@@ -262,6 +265,25 @@ def measure_config(name, rank, world, steps, warmup, dev, flush, split="native",
     res = {"name": name, "t_ms": t_ms, "t_min_ms": float(np.min(per)), "unique_bytes": unique,
            "pack_ms": pack_ms, "info": info, "launches_per_step": _launches(plan), "kvh": kvh, "hq": hq}
     if with_e2e:
+        # the dominant kernel alone (the forward; same plan without the merge launch),
+        # CUDA events on the launching stream, same L2 flush: roofline.achieved
+        fplan = P.PatPlan.from_table(table, hq, kvh, w.head_dim, split=split, forward_only=True)
+        fgraph = P.PatLayerGraph(fplan, q, kc, vc, out=torch.empty_like(q), workspace=ws)
+        for _ in range(warmup):
+            flush.zero_()
+            fgraph.replay()
+        fevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        torch.cuda.synchronize(dev)
+        for i in range(steps):
+            flush.zero_()
+            fevs[i][0].record(stream)
+            fgraph.replay()
+            fevs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        res["fwd_ms"] = float(np.mean([a.elapsed_time(b) for a, b in fevs]))
+        del fgraph
+        fplan.close()
+    if with_e2e:
         res["e2e"] = measure_e2e(P, plan, w, table, q, kc, vc, ws, steps, warmup, dev, flush)
     plan.close()
     del kc, vc
@@ -379,6 +401,7 @@ def main():
         return float(t.item())
 
     t_ms = reduce_max(main_res["t_ms"])
+    fwd_ms = reduce_max(main_res["fwd_ms"])
     tot_bytes = reduce_sum(main_res["unique_bytes"])
     e2e_ms = reduce_max(main_res["e2e"]["t_ms"])
     other_summary = {}
@@ -402,6 +425,7 @@ def main():
     traffic = load_traffic(args.config) if world == 1 else None
     if rank == 0:
         gbs = tot_bytes / (t_ms * 1e-3) / 1e9
+        fwd_gbs = tot_bytes / (fwd_ms * 1e-3) / 1e9
         info = main_res["info"]
         clocks = sampler.summary()
         line = {
@@ -414,13 +438,18 @@ def main():
                        "split": args.split, "l2": "flushed before every step (512 MB write)",
                        "unique_kv_bytes": int(tot_bytes), "packs": info.n_packs, "units": info.n_units,
                        "work_items": info.n_items, "merge_queries": info.n_merge_q},
-            "roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": round(gbs / peaks["hbm_gbs"], 4),
+            "roofline": {"bound": "hbm", "achieved": round(fwd_gbs, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(fwd_gbs / peaks["hbm_gbs"], 4),
+                         "kernel_us": round(fwd_ms * 1e3, 2),
+                         "layer_GBps": round(gbs, 2), "layer_frac": round(gbs / peaks["hbm_gbs"], 4),
                          "traffic": traffic["bytes"] if traffic else None,
+                         "layer_traffic": traffic["layer_bytes"] if traffic else None,
                          "traffic_source": traffic["source"] if traffic else None,
-                         "kernel": "one decode-attention layer replayed as a CUDA graph: the forward kernel (tcgen05 "
-                                   "fwd_tc2_kernel; fwd_stream_kernel for all-narrow plans) + merge_kernel; achieved = "
-                                   "unique KV bytes / layer time; traffic = DRAM read+write of the layer's kernels (ncu)",
+                         "kernel": "dominant kernel = the forward (tcgen05 fwd_tc2_kernel; fwd_stream_kernel for "
+                                   "all-narrow plans), timed live with CUDA events as a graph of the same plan without "
+                                   "the merge launch; achieved = unique KV bytes / its time; layer_* = forward + "
+                                   "merge_kernel; traffic = DRAM read+write of the forward kernel per launch, layer_traffic "
+                                   "of all the layer's kernels (ncu)",
                          "peak_source": peaks["source"]},
             "e2e": {"value": round(tot_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": main_res["e2e"]["h2d"], "d2h_bytes_per_step": main_res["e2e"]["d2h"],

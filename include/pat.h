@@ -59,7 +59,9 @@ enum pat_split_mode {
 };
 
 enum pat_plan_flags {
-  PAT_PLAN_HOST_ONLY = 1 /* build and keep the plan on the host only (no device upload) */
+  PAT_PLAN_HOST_ONLY = 1,   /* build and keep the plan on the host only (no device upload) */
+  PAT_PLAN_FORWARD_ONLY = 2 /* timing aid: pat_forward launches the forward kernel(s) but not
+                               the merge (multi-unit queries' outputs are left unwritten) */
 };
 
 typedef struct pat_plan pat_plan;

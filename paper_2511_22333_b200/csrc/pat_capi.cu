@@ -53,6 +53,7 @@ using namespace pat;
 struct pat_plan {
   int B = 0, bs = 16, H = 0, KVH = 0, d = 0, split_mode = 0, num_sms = 148, tc_min_rows = 64;
   bool tc_auto = false;  // tc_min_rows left to the library (options value 0)
+  bool forward_only = false;  // PAT_PLAN_FORWARD_ONLY
   bool on_device = false;
   HostPacks packs;
   HostSchedule sched;
@@ -104,6 +105,7 @@ void init_plan(pat_plan* P, int B, int bs, const pat_plan_options* opt) {
   P->split_mode = opt->split_mode;
   P->num_sms = opt->num_sms;
   P->tc_auto = opt->tc_min_rows == 0;
+  P->forward_only = (opt->flags & PAT_PLAN_FORWARD_ONLY) != 0;
   P->tc_min_rows = opt->tc_min_rows == 0 ? 1 : (opt->tc_min_rows < 0 ? 0 : opt->tc_min_rows);
   if (P->d != 64 && P->d != 128) P->tc_min_rows = 0;
   if (P->num_sms <= 0) {
@@ -455,7 +457,7 @@ int pat_forward(const pat_plan* Pc, const void* q, const void* k_cache, const vo
     }
     for (int i = 1; i < na; ++i) CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join[active[i]], 0));
   }
-  if (P->n_merge > 0) {
+  if (P->n_merge > 0 && !P->forward_only) {
     int warps = P->n_merge * P->H;
     int grid = std::max(1, std::min((warps + 7) / 8, P->num_sms * 8));
     CUDA_TRY(launch_merge(P->dev, grid, dtype, P->d, po, pl, out, st));

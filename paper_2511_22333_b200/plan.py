@@ -36,18 +36,19 @@ class PatPlan:
 
     # -- construction ---------------------------------------------------------------
     @staticmethod
-    def _opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms=0, tc_min_rows=0):
+    def _opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms=0, tc_min_rows=0, forward_only=False):
         if split not in N.SPLIT_MODES:
             raise InvalidSpec(f"split must be one of {sorted(N.SPLIT_MODES)}")
-        return N.PlanOptions(num_heads, num_kv_heads, head_dim, N.SPLIT_MODES[split], num_sms,
-                             N.PAT_PLAN_HOST_ONLY if host_only else 0, tc_min_rows)
+        flags = (N.PAT_PLAN_HOST_ONLY if host_only else 0) | (N.PAT_PLAN_FORWARD_ONLY if forward_only else 0)
+        return N.PlanOptions(num_heads, num_kv_heads, head_dim, N.SPLIT_MODES[split], num_sms, flags, tc_min_rows)
 
     @classmethod
     def from_table(cls, table, num_heads=32, num_kv_heads=8, head_dim=128, split="native", host_only=False,
-                   num_sms=0, tc_min_rows=0) -> "PatPlan":
-        """Host C++ packer (``pat_plan_create_host``) on a BlockTable."""
+                   num_sms=0, tc_min_rows=0, forward_only=False) -> "PatPlan":
+        """Host C++ packer (``pat_plan_create_host``) on a BlockTable.  ``forward_only``:
+        timing aid, ``pat_forward`` skips the merge."""
         off, blk, valid = table.csr()
-        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms, tc_min_rows)
+        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms, tc_min_rows, forward_only)
         h = C.c_void_p()
         st = N.lib().pat_plan_create_host(len(table.rows), N.ptr(off, C.c_int64), N.ptr(blk, C.c_int32),
                                           N.ptr(valid, C.c_int32), table.block_size, C.byref(opt), C.byref(h))
