@@ -124,13 +124,21 @@ class PatDecoder:
 
     def plan_for_device(self, block_tables, seq_lens, block_size: int = 16) -> PatPlan:
         """Lazy update for device tables: reuse the plan while the device fingerprint
-        is unchanged, else re-plan with the GPU packer (``pat_plan_create_device``)."""
+        is unchanged, else re-plan with the GPU packer (``pat_plan_create_device``).
+        Every layer of a decode step passes the same (unmodified) table tensors: those
+        calls skip even the fingerprint (tensor identity + autograd version counter)."""
+        ident = (block_tables.data_ptr(), block_tables._version, tuple(block_tables.shape), seq_lens.data_ptr(),
+                 seq_lens._version, block_size)
+        last = getattr(self, "_last_dev", None)
+        if last is not None and last[0] == ident and last[1]._h:
+            return last[1]
         key = f"dev:{self.table_hash(block_tables, seq_lens, block_size):016x}"
         plan = self.cache.lookup(key)
         if plan is None:
             plan = PatPlan.from_device_table(block_tables, seq_lens, block_size, self.num_heads, self.num_kv_heads,
                                              self.head_dim, split=self.split, tc_min_rows=self.tc_min_rows)
             self.cache.store(key, plan)
+        self._last_dev = (ident, plan)
         return plan
 
     def forward_device(self, block_tables, seq_lens, q, k_cache, v_cache, out=None, scale=None):

@@ -91,8 +91,11 @@ def test_device_lazy_update():
     h0 = dec.table_hash(bt, sl)
     assert dec.table_hash(bt.clone(), sl.clone()) == h0
     out_dev = dec.forward_device(bt, sl, q, kc, vc).clone()
-    out_dev2 = dec.forward_device(bt, sl, q, kc, vc)
+    out_dev2 = dec.forward_device(bt, sl, q, kc, vc).clone()  # same tensors: identity fast path
+    assert dec.cache.hits == 0 and dec.cache.misses == 1
+    out_dev3 = dec.forward_device(bt.clone(), sl.clone(), q, kc, vc)  # equal table: fingerprint hit
     assert dec.cache.hits == 1 and dec.cache.misses == 1
+    assert torch.equal(out_dev3, out_dev)
     out_host = dec(table, q, kc, vc)
     torch.cuda.synchronize()
     assert torch.equal(out_dev, out_dev2) and torch.equal(out_dev, out_host)
@@ -127,3 +130,27 @@ def test_torch_op_decode_attention():
     ref = P.pat_attention(plan, q, kv[0].contiguous(), kv[1].contiguous())
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_vllm_backend_decode_matches_pat():
+    """PatAttentionImpl (vLLM CUSTOM backend) on a decode-only batch == pat_attention."""
+    vllm_backend = pytest.importorskip("paper_2511_22333_b200.vllm_backend")
+    from types import SimpleNamespace
+
+    w = configs.workload("c2")
+    table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    bt_np, sl_np = table.padded()
+    g = torch.Generator(device="cuda").manual_seed(13)
+    nb = w.num_pool_blocks()
+    kv = torch.randn(2, nb, 16, 8, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    q = torch.randn(w.batch, 32, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    impl = vllm_backend.PatAttentionImpl(32, 128, 128 ** -0.5, 8, None, None, "auto")
+    meta = SimpleNamespace(max_query_len=1, use_cascade=False, num_actual_tokens=w.batch,
+                           block_table=torch.from_numpy(bt_np).cuda(), seq_lens=torch.from_numpy(sl_np).cuda())
+    output = torch.empty(w.batch, 32 * 128, device="cuda", dtype=torch.bfloat16)
+    impl.forward(None, q.view(w.batch, -1), None, None, kv, meta, output)
+    impl.forward(None, q.view(w.batch, -1), None, None, kv, meta, output)  # plan reused (identity fast path)
+    plan = PatPlan.from_table(table, 32, 8, 128)
+    ref = P.pat_attention(plan, q, kv[0], kv[1])
+    torch.cuda.synchronize()
+    assert torch.equal(output.view(w.batch, 32, 128), ref)
