@@ -154,3 +154,17 @@ def test_vllm_backend_decode_matches_pat():
     ref = P.pat_attention(plan, q, kv[0], kv[1])
     torch.cuda.synchronize()
     assert torch.equal(output.view(w.batch, 32, 128), ref)
+
+
+def test_cli_run_and_verify(tmp_path, capsys):
+    """B200 rows for the reference CLI: verify passes, run reports all strategies."""
+    import json as _json
+    from paper_2511_22333_b200 import cli
+    spec = tmp_path / "w.json"
+    spec.write_text(_json.dumps(P.WorkloadSpec((1, 4), (256, 64), num_heads=32, num_kv_heads=8,
+                                               head_dim=128).to_json()))
+    assert cli.main(["verify", str(spec)]) == cli.EXIT_OK
+    assert cli.main(["run", "--config", "c1", "--verify"]) == cli.EXIT_OK
+    rows = _json.loads(capsys.readouterr().out.split("\n", 1)[1])
+    assert [r["strategy"] for r in rows] == list(cli.STRATEGIES) and all(r["verified"] for r in rows)
+    assert rows[0]["kv_bytes"] < rows[1]["kv_bytes"]  # packing streams fewer KV bytes than query-centric

@@ -179,3 +179,12 @@ def test_torch_op_registered():
     import torch
     import paper_2511_22333_b200  # noqa: F401
     assert hasattr(torch.ops.patb200, "decode_attention")
+
+
+def test_cli_invalid_spec_exit_code(tmp_path):
+    """Reference exit-code contract (cli.py:24-27): unreadable spec -> 2."""
+    from paper_2511_22333_b200 import cli
+    bad = tmp_path / "w.json"
+    bad.write_text('{"group_sizes": [0], "segment_lens": [16]}')
+    assert cli.main(["verify", str(bad)]) == cli.EXIT_INVALID_SPEC
+    assert cli.main(["run"]) == cli.EXIT_INVALID_SPEC
