@@ -34,13 +34,14 @@ namespace tc2 {
 
 #ifdef PAT_TC_TRACE
 // Debug timeline (tools/tc_trace.py): CTA 0 records clock64 per (role, event, step).
-// roles: 0 producer, 1 MMA issuer, 2 softmax (warp 2 lane 0), 3 unused.
+// roles: 0 producer, 1 MMA issuer, 2 softmax (warp 2 lane 0), 3 softmax epilogue.
 constexpr int kTraceSteps = 256;
 __device__ long long g_tc_trace[4][8][kTraceSteps];
+__device__ int g_trace_cta;  // the CTA traced (pat_debug_trace_cta)
 __device__ unsigned long long g_span_tc[1][kSpanCtas][2];
 #define TC_TRACE(role, ev, step)                                                         \
   do {                                                                                   \
-    if (blockIdx.x == 0 && (step) < kTraceSteps) g_tc_trace[role][ev][step] = clock64(); \
+    if (blockIdx.x == g_trace_cta && (step) < kTraceSteps) g_tc_trace[role][ev][step] = clock64(); \
   } while (0)
 #else
 #define TC_TRACE(role, ev, step) \
@@ -551,11 +552,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float l = (lds_f32(red_at(xc & 1, 0)) + lds_f32(red_at(xc & 1, 1))) +
                       (lds_f32(red_at(xc & 1, 2)) + lds_f32(red_at(xc & 1, 3)));
       ++xc;
+      if (tr) TC_TRACE(3, 0, g - 1);
       const bool live = t < fld(n, kFNrows);
       const int2 meta = live ? lds_v2(ring_s + (n & 1) * kSlotBytes + kFMeta + 8 * t) : make_int2(0, -1);
       const int head = fld(n, kFKvh) * G + (live ? (fld(n, kFRow0) + t) % G : 0);
       mbar_wait(bar(P_FREE + ((c - 1) & 1)), ((c - 1) >> 1) & 1);  // last PV done
       tc_fence_after();
+      if (tr) TC_TRACE(3, 1, g - 1);
       const float inv = 1.f / l;
 #pragma unroll
       for (int q = 0; q < kOCols / 16; ++q) {
@@ -582,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (live && meta.y >= 0 && cq == 0) part_lse[(int64_t)meta.y * H + head] = m_ref + log2f(l);
+      if (tr) TC_TRACE(3, 2, g - 1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(O_EMPTY));
@@ -661,6 +665,11 @@ static cudaError_t launch_tc2_t(const CUtensorMap& tmk, const CUtensorMap& tmv, 
 #ifdef PAT_TC_TRACE
 extern "C" int pat_debug_tc_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, tc2::g_tc_trace, sizeof(tc2::g_tc_trace));
+}
+extern "C" int pat_debug_trace_cta(int cta) {
+  static long long zero[4][8][tc2::kTraceSteps];
+  cudaMemcpyToSymbol(tc2::g_tc_trace, zero, sizeof(zero));
+  return (int)cudaMemcpyToSymbol(tc2::g_trace_cta, &cta, sizeof(int));
 }
 extern "C" int pat_debug_spans_tc(unsigned long long* host) {
   int e = (int)cudaMemcpyFromSymbol(host, tc2::g_span_tc, sizeof(tc2::g_span_tc));

@@ -60,10 +60,21 @@ __global__ void __launch_bounds__(128, 1) probe(int reps, long long* out) {
         } else if (MODE == 1) {
           uint64_t b = umma_desc_sw128(sb + 49152 + (k & 3) * 16 * 128, 64 * 128, 1024);
           umma_f16_ts(tmem + 256, tmem + 128 + k * 8, b, id_pv, 1u);
-        } else {
+        } else if (MODE == 2) {
           uint64_t a = umma_desc_sw128(sb + kb * 16384 + kk * 32, 16, 1024);
           uint64_t b = umma_desc_sw128(sb + 32768 + kb * 16384 + kk * 32, 16, 1024);
           umma_f16_ss(tmem, a, b, id_qk128, 1u);
+        } else if (MODE == 3) {
+          uint64_t b = umma_desc_sw128(sb + 49152 + (k & 3) * 16 * 128, 64 * 128, 1024);
+          umma_f16_ts(tmem + 256, tmem + 128 + k * 8, b, umma_idesc_f16(64, 128, 1, 1), 1u);
+        } else if (MODE == 4) {
+          uint64_t a = umma_desc_sw128(sb + kb * 16384 + kk * 32, 16, 1024);
+          uint64_t b = umma_desc_sw128(sb + 32768 + kb * 8192 + kk * 32, 16, 1024);
+          umma_f16_ss(tmem, a, b, umma_idesc_f16(64, 64, 1, 0), 1u);
+        } else {
+          uint64_t a = umma_desc_sw128(sb + kb * 16384 + kk * 32, 16, 1024);
+          uint64_t b = umma_desc_sw128(sb + 49152 + (k & 3) * 16 * 128, 64 * 128, 1024);
+          umma_f16_ss(tmem + 256, a, b, umma_idesc_f16(64, 128, 1, 1), 1u);
         }
       }
     }
@@ -108,6 +119,9 @@ int main() {
     run<0>("QK SS M128 N64", grid);
     run<1>("PV TS M128 N128", grid);
     run<2>("QK SS M128 N128", grid);
+    run<4>("QK SS M64 N64", grid);
+    run<5>("PV SS M64 N128", grid);
+    run<3>("PV TS M64 N128", grid);
   }
   return 0;
 }

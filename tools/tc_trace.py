@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--steps", type=int, default=24)
     ap.add_argument("--lib", default=TRACE_LIB)
     ap.add_argument("--dtype", default="bfloat16")
-    ap.add_argument("--config", default=None, help="trace CTA 0 of a BASELINE config layer instead")
+    ap.add_argument("--config", default=None, help="trace a CTA of a BASELINE config layer instead")
+    ap.add_argument("--cta", type=int, default=0, help="CTA to trace")
     args = ap.parse_args()
     if args.build:
         from paper_2511_22333_b200 import build as B
@@ -65,8 +66,12 @@ def main():
     out = torch.empty_like(q)
     ws = torch.empty(max(plan.workspace_bytes(), 256), dtype=torch.uint8, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    lib0 = N.lib()
+    lib0.pat_debug_trace_cta.argtypes = [C.c_int]
     times = []
     for i in range(6):
+        if i == 5:
+            lib0.pat_debug_trace_cta(args.cta)
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -90,7 +95,7 @@ def main():
              (2, 4): "smA_qstored", (2, 0): "smA_sfull", (2, 6): "smA_sloaded", (2, 7): "smA_maxed",
              (2, 1): "smA_exp_done", (2, 2): "smA_odone",
              (2, 3): "smA_pfull", (2, 5): "smA_epi_done",
-             (3, 0): "sm_nextitem", (3, 1): "sm_qloads_issued", (3, 2): "sm_qempty"}
+             (3, 0): "epi_lexch", (3, 1): "epi_pvdone", (3, 2): "epi_stored"}
     hdr = " step " + " ".join(f"{v:>15s}" for v in names.values())
     print(hdr)
     n = min(args.steps, ntok // 64) if ntok else args.steps
@@ -100,6 +105,15 @@ def main():
             v = tr[r, e, s]
             row.append(f"{(v - t0) if v else -1:>15d}")
         print(f"{s:5d} " + " ".join(row))
+    # item boundaries: the last step's P, the epilogue phases, the next item's first S
+    print("item boundaries (cycles since the first producer event):")
+    print("  step  pfull(last)  epi_lexch  epi_pvdone  epi_stored  epi_done  next:qfull  next:kvfull  next:qk_issued  next:sfull")
+    for s in range(n):
+        if tr[2, 5, s] <= 0 or s + 1 >= 256:
+            continue
+        f = lambda r, e, k: (tr[r, e, k] - t0) if tr[r, e, k] > 0 else -1
+        print(f"  {s:4d} {f(2, 3, s):12d} {f(3, 0, s):10d} {f(3, 1, s):11d} {f(3, 2, s):11d} {f(2, 5, s):9d}"
+              f" {f(1, 5, s + 1):11d} {f(1, 0, s + 1):12d} {f(1, 1, s + 1):15d} {f(2, 0, s + 1):11d}")
     # steady-state per-step cycles from the MMA issuer's KV_FULL timestamps
     m = tr[1, 0, :n]
     m = m[m > 0]
