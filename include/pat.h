@@ -135,6 +135,27 @@ int pat_plan_export_packs(const pat_plan* plan, int32_t* q_off, int32_t* q_ids, 
 int pat_plan_export_units(const pat_plan* plan, int32_t* pack, int32_t* page0, int32_t* npages,
                           int32_t* ntok, int32_t* split_index, int32_t* split_of);
 
+/* Scheduler cost model (ns): the native KV split and the longest-first item
+ * order estimate a work item of `rows` rows over `steps` 64-token KV tiles as
+ *   tcgen05:   tc_item_ns + tc_item_row_ns * rows / 128 + steps * tc_step_ns * (0.5 + 0.5 * d / 128)
+ *   streaming: stream_item_ns + steps * 64 * d * 4 / (hbm_bytes_per_ns / num_sms)
+ * and the layer's byte floor as bytes / hbm_bytes_per_ns.  Process-wide; read
+ * when a plan is created.  Defaults are the hand-tuned round-1 constants;
+ * tools/calibrate.py measures the B200 values (profiles/b200_calibration.json,
+ * loaded by paper_2511_22333_b200.calibration.load_profile).  Replaces the
+ * reference's A100 tile cost tables (tiles.py). */
+typedef struct pat_cost_model {
+  double tc_item_ns;
+  double tc_item_row_ns;
+  double tc_step_ns;
+  double stream_item_ns;
+  double hbm_bytes_per_ns;
+} pat_cost_model;
+
+/* PAT_ERR_INVALID_SPEC on a NULL pointer or a non-positive step / bandwidth. */
+int pat_set_cost_model(const pat_cost_model* model);
+int pat_get_cost_model(pat_cost_model* model);
+
 /* Bytes of device workspace pat_forward needs (fp32 partials + counters). */
 size_t pat_workspace_bytes(const pat_plan* plan);
 

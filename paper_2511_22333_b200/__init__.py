@@ -18,6 +18,7 @@ from .packer import (CtaTask, PackCache, baseline_query_centric, naive_per_node,
 from .plan import PatPlan
 from .attention import PatDecoder, PatLayerGraph, kv_pool_from_store, pat_attention, run_packed_attention
 from .metrics import distinct_block_census, theoretical_min_kv_bytes
+from .calibration import CostModel, get_cost_model, load_profile, set_cost_model
 from .torch_op import decode_attention  # registers torch.ops.patb200.decode_attention
 
 __version__ = "0.1.0"

@@ -37,8 +37,15 @@ class PlanInfo(C.Structure):
                 ("n_fwd_kernels", C.c_int32), ("n_launches", C.c_int32)]
 
 
+class CostModel(C.Structure):
+    _fields_ = [("tc_item_ns", C.c_double), ("tc_item_row_ns", C.c_double), ("tc_step_ns", C.c_double),
+                ("stream_item_ns", C.c_double), ("hbm_bytes_per_ns", C.c_double)]
+
+
 # (name, restype, argtypes) -- the complete exported surface of include/pat.h
 SIGNATURES = [
+    ("pat_set_cost_model", C.c_int, [C.POINTER(CostModel)]),
+    ("pat_get_cost_model", C.c_int, [C.POINTER(CostModel)]),
     ("pat_plan_create_host", C.c_int, [C.c_int32, i64p, i32p, i32p, C.c_int32, C.POINTER(PlanOptions),
                                        C.POINTER(C.c_void_p)]),
     ("pat_table_hash_device", C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p,

@@ -39,5 +39,7 @@ struct ScheduleParams {
   int tc_min_rows;  // rows threshold of the tcgen05 variant (0 = off)
 };
 int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* out);
+// process-wide scheduler cost model (pat_set_cost_model)
+const pat_cost_model& cost_model();
 
 }  // namespace pat

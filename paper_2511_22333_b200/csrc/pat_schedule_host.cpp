@@ -9,10 +9,17 @@
 #include <numeric>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "pat_plan_host.h"
 
 namespace pat {
+
+// Hand-tuned round-1 constants (see DESIGN.md §4.7 for the measured fits).
+static pat_cost_model g_cost_model = {3000.0, 0.0, 700.0, 1500.0, 6.0e3};
+static std::mutex g_cost_mu;
+
+const pat_cost_model& cost_model() { return g_cost_model; }
 
 namespace {
 
@@ -41,11 +48,12 @@ void split_pack(int npages, int kv, int bs, int parts, std::vector<Part>& out) {
 // item's KV and Q latency, epilogue); the mma.sync streaming kernel is
 // HBM-paced.
 double item_ns(const ScheduleParams& sp, int v, int rows, int ntok) {
+  const pat_cost_model& cm = cost_model();
   const double steps = (double)ceil_div(ntok, 64);
   const double dscale = sp.d / 128.0;
-  if (v == VAR_TC) return 3000.0 + steps * 700.0 * (0.5 + 0.5 * dscale);
-  const double bw = 6.0e3;  // bytes per ns (HBM, sustained)
-  return 1500.0 + steps * 64.0 * sp.d * 4 / (bw / std::max(sp.num_sms, 1));
+  if (v == VAR_TC)
+    return cm.tc_item_ns + cm.tc_item_row_ns * rows / 128.0 + steps * cm.tc_step_ns * (0.5 + 0.5 * dscale);
+  return cm.stream_item_ns + steps * 64.0 * sp.d * 4 / (cm.hbm_bytes_per_ns / std::max(sp.num_sms, 1));
 }
 
 // Native KV split for B200.  Picks one chunk size (pages) for all packs by
@@ -57,7 +65,7 @@ double item_ns(const ScheduleParams& sp, int v, int rows, int ntok) {
 void native_parts(const HostPacks& P, const ScheduleParams& sp, std::vector<int>& nparts) {
   const int NP = P.n_packs();
   const int G = sp.H / sp.KVH;
-  const double bw = 6.0e3;  // bytes per ns (HBM, sustained)
+  const double bw = cost_model().hbm_bytes_per_ns;
   std::vector<int> rows(NP), pages(NP);
   int maxpages = 1;
   double kv_bytes = 0;
@@ -224,3 +232,19 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S)
 }
 
 }  // namespace pat
+
+extern "C" int pat_set_cost_model(const pat_cost_model* m) {
+  if (!m || !(m->tc_step_ns > 0) || !(m->hbm_bytes_per_ns > 0) || m->tc_item_ns < 0 || m->tc_item_row_ns < 0 ||
+      m->stream_item_ns < 0)
+    return PAT_ERR_INVALID_SPEC;
+  std::lock_guard<std::mutex> lk(pat::g_cost_mu);
+  pat::g_cost_model = *m;
+  return PAT_OK;
+}
+
+extern "C" int pat_get_cost_model(pat_cost_model* m) {
+  if (!m) return PAT_ERR_INVALID_SPEC;
+  std::lock_guard<std::mutex> lk(pat::g_cost_mu);
+  *m = pat::g_cost_model;
+  return PAT_OK;
+}

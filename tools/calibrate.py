@@ -11,7 +11,8 @@ evenly loaded), timed as a CUDA graph with L2 flushed:
 * `items`: the same 64 tiles per SM cut into 2 / 4 / 8 / 16 / 32 items ->
   the cost of an item boundary (`per_item_us`).
 
-The constants of `item_ns` in csrc/pat_schedule_host.cpp follow these fits."""
+`paper_2511_22333_b200.calibration.load_profile(path)` turns the fits into the
+scheduler's cost model (`pat_set_cost_model`)."""
 
 import argparse
 import json
