@@ -52,7 +52,10 @@ constexpr int kThreads = 576;  // producer, MMA issuer (+TMEM alloc), 16 softmax
 constexpr int kSoftWarps = 16;
 constexpr int kM = 128;        // rows per item tile (TMEM lanes)
 constexpr int kN = 64;         // tokens per KV tile
-constexpr int kStages = 6;
+#ifndef PAT_TC_STAGES
+#define PAT_TC_STAGES 6
+#endif
+constexpr int kStages = PAT_TC_STAGES;  // KV ring depth (6 x 32 KB fills the shared memory)
 constexpr uint32_t kTmemCols = 512;
 #ifndef PAT_TC_RESCALE_THRESHOLD
 #define PAT_TC_RESCALE_THRESHOLD 8.0f
