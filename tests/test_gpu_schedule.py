@@ -82,3 +82,24 @@ def test_concurrent_kernels_vs_oracle(tc):
     torch.cuda.synchronize()
     _check_sampled(w, q, kc, vc, out, [0, 17, 40, 63])
     plan.close()
+
+
+def test_calibrated_cost_model_plans_vs_oracle():
+    """The measured B200 profile (tools/calibrate.py) installed as the cost model
+    re-chunks the plan; the layer still matches the oracle on sampled queries."""
+    import os
+
+    from paper_2511_22333_b200 import calibration as CAL
+
+    saved = CAL.get_cost_model()
+    try:
+        CAL.load_profile(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                                      "b200_calibration.json"))
+        w, table, q, kc, vc = _setup("c3", seed=5)
+        plan = PatPlan.from_table(table, w.num_heads, w.num_kv_heads, w.head_dim)
+        out = P.pat_attention(plan, q, kc, vc)
+        torch.cuda.synchronize()
+        _check_sampled(w, q, kc, vc, out, random.Random(5).sample(range(w.batch), 6))
+        plan.close()
+    finally:
+        CAL.set_cost_model(saved)
