@@ -1,7 +1,7 @@
 // Tensor-core (tcgen05 + TMEM + TMA) forward kernel: one persistent CTA per SM
 // pulls work items (unit x kv head x up-to-128 rows) from a global counter in
 // the scheduler's longest-first order and streams each item's KV span once
-// through a 6-stage TMA ring.  Every pack goes through it: a narrow pack (a few
+// through a 5-stage TMA ring.  Every pack goes through it: a narrow pack (a few
 // queries x G heads) still runs QK^T / PV on the tensor core (M = 128 rows, the
 // padding rows are free: the kernel is HBM- or softmax-bound, never MMA-bound).
 //
@@ -53,9 +53,9 @@ constexpr int kSoftWarps = 16;
 constexpr int kM = 128;        // rows per item tile (TMEM lanes)
 constexpr int kN = 64;         // tokens per KV tile
 #ifndef PAT_TC_STAGES
-#define PAT_TC_STAGES 6
+#define PAT_TC_STAGES 5
 #endif
-constexpr int kStages = PAT_TC_STAGES;  // KV ring depth (6 x 32 KB fills the shared memory)
+constexpr int kStages = PAT_TC_STAGES;  // KV ring depth: 4-6 measure the same; 5 is ~1% faster on c3 / c4
 constexpr uint32_t kTmemCols = 512;
 #ifndef PAT_TC_RESCALE_THRESHOLD
 #define PAT_TC_RESCALE_THRESHOLD 8.0f
