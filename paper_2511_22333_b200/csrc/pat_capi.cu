@@ -10,6 +10,7 @@
 #include <vector>
 
 #include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "pat_plan_host.h"
 
@@ -31,11 +32,41 @@ cudaError_t launch_merge(const DevPlan& plan, int grid, int dtype, int d, const 
                          void* out, cudaStream_t st);
 cudaError_t launch_forward_tc(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var, int grid,
                               int dtype, int d, const void* q, void* out, float* po, float* pl, float scale_log2,
-                              cudaStream_t st);
-int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t num_blocks, int bs, int kvh, int d, int dtype);
+                              int32_t* sched, cudaStream_t st);
 int device_pack(const int32_t* d_bt, int64_t stride, const int32_t* d_seq, int B, int maxb, int bs, cudaStream_t st,
                 HostPacks* out, std::vector<int32_t>* h_nblk, std::vector<int32_t>* h_valid,
                 std::vector<int32_t>* h_rows);
+
+// ------------------------------------------------------------------------------------------
+// TMA descriptors over the paged cache
+// ------------------------------------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 4-D map over a paged cache [num_blocks][bs][KVH][D]: box (64 d, 1 head, 16 tokens, 1 block).
+int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t num_blocks, int bs, int kvh, int d, int dtype) {
+  auto enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)kvh, (cuuint64_t)bs, (cuuint64_t)num_blocks};
+  cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)kvh * d * 2, (cuuint64_t)bs * kvh * d * 2};
+  cuuint32_t box[4] = {64, 1, 16, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, dtype == PAT_DTYPE_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
 
 }  // namespace pat
 
@@ -432,7 +463,8 @@ int pat_forward(const pat_plan* Pc, const void* q, const void* k_cache, const vo
   auto launch = [&](int v, cudaStream_t sv) -> cudaError_t {
     const int grid = grid_of(v);
     if (v == VAR_TC)
-      return launch_forward_tc(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sv);
+      return launch_forward_tc(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2,
+                               P->dev.sched, sv);
     return launch_forward_variant(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sv);
   };
   if (na == 1) {

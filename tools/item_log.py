@@ -1,0 +1,90 @@
+"""Per-item timeline of the tcgen05 forward kernel over a whole layer (all CTAs).
+
+    python tools/tc_trace.py --build                 # here: tools/libpat_trace.so (-DPAT_TC_TRACE)
+    python tools/item_log.py c2 [c4 ...]              # on the GPU box
+
+For every work item the first softmax thread of CTA c records globaltimer at
+item start, first KV/S data ready, tile loop done and epilogue done
+(`g_item_log`).  Prints, per config: the layer span, the per-CTA split into
+item start latency / tiles / epilogue / idle tail, per-tile ns by item kind,
+and the slowest CTAs.  A debugging tool, not a bench number."""
+
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+os.environ.setdefault("PAT_LIB", os.path.join(REPO, "tools", "libpat_trace.so"))
+
+import paper_2511_22333_b200 as P  # noqa: E402
+from paper_2511_22333_b200 import _native as N  # noqa: E402
+from paper_2511_22333_b200 import configs  # noqa: E402
+
+
+def run(name, tc_min_rows=0):
+    w = configs.workload(name)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    nb, dt = w.num_pool_blocks(), torch.bfloat16
+    kc = torch.randn(nb, w.block_size, w.num_kv_heads, w.head_dim, device="cuda", dtype=dt, generator=g)
+    vc = torch.randn(nb, w.block_size, w.num_kv_heads, w.head_dim, device="cuda", dtype=dt, generator=g)
+    q = torch.randn(w.batch, w.num_heads, w.head_dim, device="cuda", dtype=dt, generator=g)
+    table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    plan = P.PatPlan.from_table(table, w.num_heads, w.num_kv_heads, w.head_dim, tc_min_rows=tc_min_rows,
+                                forward_only=True)
+    out = torch.empty_like(q)
+    ws = torch.zeros(max(plan.workspace_bytes(), 256), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    lib = N.lib()
+    lib.pat_debug_item_log.argtypes = [C.c_void_p, C.c_void_p]
+    log = np.zeros((32768, 8), dtype=np.int64)
+    cnt = np.zeros(1, dtype=np.int32)
+    for i in range(4):
+        flush.zero_()
+        torch.cuda.synchronize()
+        lib.pat_debug_item_log(log.ctypes.data, cnt.ctypes.data)  # clears
+        P.pat_attention(plan, q, kc, vc, out=out, workspace=ws)
+        torch.cuda.synchronize()
+    lib.pat_debug_item_log(log.ctypes.data, cnt.ctypes.data)
+    n = int(cnt[0])
+    e = log[:n]
+    t0 = e[:, 4].min()
+    end = e[:, 7].max()
+    span = (end - t0) / 1e3
+    start_lat = (e[:, 5] - e[:, 4]) / 1e3
+    tiles = (e[:, 6] - e[:, 5]) / 1e3
+    epi = (e[:, 7] - e[:, 6]) / 1e3
+    print(f"== {name}: {n} items, layer span {span:.1f} us (first item start -> last epilogue)")
+    ncta = int(e[:, 0].max()) + 1
+    idle = np.zeros(ncta)
+    first = np.zeros(ncta)
+    for c in range(ncta):
+        m = e[:, 0] == c
+        if m.any():
+            idle[c] = (end - e[m, 7].max()) / 1e3
+            first[c] = (e[m, 4].min() - t0) / 1e3
+    tot = span * ncta
+    print(f"   per CTA avg: start-lat {start_lat.sum() / ncta:.1f}  tiles {tiles.sum() / ncta:.1f}  "
+          f"epilogue {epi.sum() / ncta:.1f}  idle-tail {idle.mean():.1f}  late-start {first.mean():.1f}  us "
+          f"(of {span:.1f})")
+    kinds = {"ns(<=16)": e[:, 2] <= 16, "eo(17-128)": (e[:, 2] > 16) & (e[:, 2] <= 128), "pp(>128)": e[:, 2] > 128}
+    for k, m in kinds.items():
+        if not m.any():
+            continue
+        nt = e[m, 3].sum()
+        print(f"   {k:10s}: {m.sum():5d} items {nt:6d} tiles  {tiles[m].sum() / max(nt, 1) * 1e3:7.1f} ns/tile(in-item) "
+              f" start-lat {start_lat[m].mean():.2f}  epi {epi[m].mean():.2f} us/item")
+    worst = np.argsort(-(end - np.array([e[e[:, 0] == c, 7].max() if (e[:, 0] == c).any() else end
+                                          for c in range(ncta)])))[:0]
+    del worst
+    plan.close()
+    _ = tot
+
+
+if __name__ == "__main__":
+    tc = int(os.environ.get("PAT_AB_TC", "0"))
+    for name in sys.argv[1:] or ["c2", "c3", "c4"]:
+        run(name, tc)

@@ -1,4 +1,4 @@
-"""Timeline of the tcgen05 forward kernel (CTA 0) on one wide pack.
+"""Timeline of the tcgen05 forward kernel (one CTA) on a synthetic pack or a config layer.
 
     python tools/tc_trace.py --build            # here: compile tools/libpat_trace.so (-DPAT_TC_TRACE)
     python tools/tc_trace.py [--nq 32 --G 8 --kvh 8 --ntok 8192]   # on the GPU box
@@ -89,13 +89,10 @@ def main():
     lib.pat_debug_tc_trace.argtypes = [C.c_void_p]
     assert lib.pat_debug_tc_trace(tr.ctypes.data) == 0
     t0 = tr[0, 0, 0]
-    names = {(0, 0): "prod_kvempty", (1, 5): "mma_item_qfull", (1, 0): "mma_kvfull", (1, 3): "qkA_start",
-             (1, 1): "mma_qk_issued",
-             (1, 4): "pvA_start(j-1)", (1, 2): "mma_pv_issued",
-             (2, 4): "smA_qstored", (2, 0): "smA_sfull", (2, 6): "smA_sloaded", (2, 7): "smA_maxed",
-             (2, 1): "smA_exp_done", (2, 2): "smA_odone",
-             (2, 3): "smA_pfull", (2, 5): "smA_epi_done",
-             (3, 0): "epi_lexch", (3, 1): "epi_pvdone", (3, 2): "epi_stored"}
+    names = {(0, 0): "prod_kvempty", (1, 5): "mma_item_q", (1, 0): "mma_kvfull", (1, 1): "mma_qk_issued",
+             (1, 4): "mma_pv_start", (1, 2): "mma_pv_issued",
+             (2, 0): "sm_sfull", (2, 6): "sm_sloaded", (2, 7): "sm_maxed", (2, 1): "sm_exp_done",
+             (2, 3): "sm_pfull", (3, 1): "epi_pvdone", (3, 2): "epi_done"}
     hdr = " step " + " ".join(f"{v:>15s}" for v in names.values())
     print(hdr)
     n = min(args.steps, ntok // 64) if ntok else args.steps
@@ -105,15 +102,6 @@ def main():
             v = tr[r, e, s]
             row.append(f"{(v - t0) if v else -1:>15d}")
         print(f"{s:5d} " + " ".join(row))
-    # item boundaries: the last step's P, the epilogue phases, the next item's first S
-    print("item boundaries (cycles since the first producer event):")
-    print("  step  pfull(last)  epi_lexch  epi_pvdone  epi_stored  epi_done  next:qfull  next:kvfull  next:qk_issued  next:sfull")
-    for s in range(n):
-        if tr[2, 5, s] <= 0 or s + 1 >= 256:
-            continue
-        f = lambda r, e, k: (tr[r, e, k] - t0) if tr[r, e, k] > 0 else -1
-        print(f"  {s:4d} {f(2, 3, s):12d} {f(3, 0, s):10d} {f(3, 1, s):11d} {f(3, 2, s):11d} {f(2, 5, s):9d}"
-              f" {f(1, 5, s + 1):11d} {f(1, 0, s + 1):12d} {f(1, 1, s + 1):15d} {f(2, 0, s + 1):11d}")
     # steady-state per-step cycles from the MMA issuer's KV_FULL timestamps
     m = tr[1, 0, :n]
     m = m[m > 0]
