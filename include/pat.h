@@ -136,11 +136,13 @@ int pat_plan_export_units(const pat_plan* plan, int32_t* pack, int32_t* page0, i
                           int32_t* ntok, int32_t* split_index, int32_t* split_of);
 
 /* Scheduler cost model (ns): the native KV split and the longest-first item
- * order estimate a work item of `rows` rows over `steps` 64-token KV tiles as
+ * order estimate a work item of `rows` rows over `steps` 64-token KV spans as
  *   tcgen05:   tc_item_ns + tc_item_row_ns * rows / 128 + steps * tc_step_ns * (0.5 + 0.5 * d / 128)
+ *              (per item pipeline; two pipelines per SM; the split simulates the
+ *              kernel's longest-first claims over 2 x num_sms pipelines)
  *   streaming: stream_item_ns + steps * 64 * d * 4 / (hbm_bytes_per_ns / num_sms)
  * and the layer's byte floor as bytes / hbm_bytes_per_ns.  Process-wide; read
- * when a plan is created.  Defaults are the hand-tuned round-1 constants;
+ * when a plan is created.  Defaults are measured B200 constants;
  * tools/calibrate.py measures the B200 values (profiles/b200_calibration.json,
  * loaded by paper_2511_22333_b200.calibration.load_profile).  Replaces the
  * reference's A100 tile cost tables (tiles.py). */

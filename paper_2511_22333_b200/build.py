@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libpatb200.so")
 SOURCES = [
     "pat_capi.cu",
     "pat_fwd_mma.cu",
-    "pat_fwd_tc3.cu",
+    "pat_fwd_tc4.cu",
     "pat_packer_host.cpp",
     "pat_packer_dev.cu",
     "pat_schedule_host.cpp",

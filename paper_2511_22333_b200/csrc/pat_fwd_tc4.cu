@@ -1,0 +1,685 @@
+// Tensor-core (tcgen05 + TMEM + TMA) forward kernel: two independent item
+// pipelines ("lanes") per CTA.
+//
+// One persistent CTA per SM runs two lanes.  Each lane claims its own work items
+// (unit x kv head x up to 128 rows) from the global counter in the scheduler's
+// longest-first order and streams each item's KV span once through its own TMA
+// ring, so one lane's item boundary (Q load, last PV, O read-out and stores)
+// overlaps the other lane's tiles instead of stalling the SM:
+//
+//   warp 0 / 2   producer of lane 0 / 1: claims items, resolves per-row (query
+//                id, partial slot) into a 2-slot item ring, warms L2 with the
+//                item's Q rows, issues TMA boxes of 16-token page slices of K
+//                and V (32-token stages, 128B swizzle) straight from the paged
+//                vLLM cache;
+//   warp 1 / 3   MMA issuer of lane 0 / 1 (warp 1 also allocates TMEM):
+//                  S[b] = Q K^T   (TS: Q from TMEM, K from smem, M=128 N=32)
+//                  O   += P[b] V  (TS: P from TMEM over S[b], V from smem)
+//                with S/P double-buffered (b = tile & 1): QK of tile t+1 runs
+//                while the softmax works on tile t;
+//   warps 4-7    softmax / epilogue of lane 0, warps 8-11 of lane 1: one thread
+//                per TMEM lane = one row of the item (query x GQA head), the
+//                whole 32-column tile per thread, so a row's running max, sum
+//                and O never leave its thread: no cross-warp fold, no CTA-wide
+//                barrier anywhere in the steady state.
+//
+// TMEM (512 columns): lane L at 256 L: S/P[b] at +32 b (P = hi 16 + lo 16
+// columns of packed 16-bit pairs written over the consumed S), Q at +64
+// (packed pairs, the A operand of QK), O at +128.
+// KV tiles are 32 tokens (16 KB stages, 6 per lane): a stage is released as
+// soon as its PV completes, so more of the ring is in flight.
+// Numerics follow cta_partial (attention.py:140-163): fp32 scores and
+// accumulators, log2-domain online softmax with lazy O rescale (only when the
+// running max grows by > 8), bf16 P = hi + lo (two PV MMAs), fp16 P single and
+// normalised by the sum of the rounded weights the MMA used.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include "pat_plan.cuh"
+#include "pat_sm100.cuh"
+
+namespace pat {
+namespace tc4 {
+
+#ifdef PAT_TC_TRACE
+// Debug timeline (tools/tc_trace.py, tools/item_log.py).
+constexpr int kTraceSteps = 256;
+__device__ long long g_tc_trace[4][8][kTraceSteps];
+__device__ int g_trace_cta;
+__device__ unsigned long long g_span_tc[1][kSpanCtas][2];
+// per-item log (all CTAs, both lanes): cta*2+lane, item, rows, tiles, t_start, t_first_data, t_tiles_done, t_epi_done
+constexpr int kItemLog = 32768;
+__device__ long long g_item_log[kItemLog][8];
+__device__ int g_item_n;
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ITEM_T(var) \
+  do {              \
+    var = gtime();  \
+  } while (0)
+#define TC_TRACE(role, ev, step)                                                   \
+  do {                                                                             \
+    if (traced && (step) < kTraceSteps) g_tc_trace[role][ev][step] = clock64(); \
+  } while (0)
+#else
+#define ITEM_T(var) \
+  do {              \
+  } while (0)
+#define TC_TRACE(role, ev, step) \
+  do {                           \
+  } while (0)
+#endif
+
+constexpr int kThreads = 384;
+constexpr int kM = 128;  // rows per item (TMEM lanes)
+constexpr int kN = 32;   // tokens per KV tile
+#ifndef PAT_TC4_STAGES
+#define PAT_TC4_STAGES 6
+#endif
+constexpr int kStages = PAT_TC4_STAGES;  // per lane
+constexpr uint32_t kTmemCols = 512;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct ItemSlot {
+  int32_t idx;
+  int32_t pad[7];
+  Item item;
+  int2 meta[kM];  // (qid, slot) per row
+};
+static_assert(sizeof(ItemSlot) == 64 + 8 * kM, "ItemSlot layout");
+constexpr uint32_t kSlotBytes = sizeof(ItemSlot);
+constexpr uint32_t kFIdx = 0, kFKvh = 32 + 4, kFRow0 = 32 + 8, kFNrows = 32 + 12, kFNtok = 32 + 20, kFMeta = 64;
+
+template <int D>
+struct Layout {
+  static constexpr int KB = D / 64;
+  static constexpr int kTileBytes = KB * kN * 128;  // K or V stage tile: [KB][32 tok][128 B]
+  static constexpr int kLaneRing = kStages * 2 * kTileBytes;
+  static constexpr int kOffKV = 0;  // lane L ring at L * kLaneRing
+  static constexpr int kOffBar = 2 * kLaneRing;
+  static constexpr int kOffRing = kOffBar + 1024;  // item slots [lane][2]
+  static constexpr int kBytes = kOffRing + 4 * (int)sizeof(ItemSlot);
+  static constexpr int kAlloc = kBytes + 1024;
+  static_assert(kAlloc <= 227 * 1024, "shared memory budget");
+};
+
+enum Bar : int {
+  KV_FULL = 0,
+  KV_EMPTY = KV_FULL + kStages,
+  S_FULL = KV_EMPTY + kStages,  // [b] QK done
+  P_FULL = S_FULL + 2,          // [b] P written over S (4 warps)
+  SP_FREE = P_FULL + 2,         // [b] the PV reading P[b] completed (O updated, S/P[b] free)
+  O_EMPTY = SP_FREE + 2,        // epilogue has read O (one arrival after the lane's named barrier)
+  QT_FULL = O_EMPTY + 1,        // the item's Q rows stored in TMEM (4 warps)
+  ITEM_FULL = QT_FULL + 1,      // [slot] published by the producer (32 lanes)
+  ITEM_EMPTY = ITEM_FULL + 2,   // [slot] released by the MMA warp and the 4 softmax warps
+  BARS_PER_LANE = ITEM_EMPTY + 2
+};
+static_assert(2 * BARS_PER_LANE * 8 + 8 <= 1024, "barrier area");
+
+template <typename T> struct Fmt;
+template <> struct Fmt<__half> {
+  static constexpr int ab = 0;
+  static constexpr bool kSplit = false;
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ float2 unpack(uint32_t v) {
+    return __half22float2(*reinterpret_cast<__half2*>(&v));
+  }
+};
+template <> struct Fmt<__nv_bfloat16> {
+  static constexpr int ab = 1;
+#ifdef PAT_TC_NO_SPLIT
+  static constexpr bool kSplit = false;
+#else
+  static constexpr bool kSplit = true;
+#endif
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ float2 unpack(uint32_t v) {
+    return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
+  }
+};
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int2 lds_v2(uint32_t a) {
+  int2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ Item load_item(const Item* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  int4 a = __ldg(q), b = __ldg(q + 1);
+  return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+}
+
+template <int D, typename T>
+// 12 warps x 168 registers (no setmaxnreg: a 56-register control warpgroup
+// spilled the MMA issuer's loop state to local memory)
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_tc4_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, DevPlan plan,
+                   int var, const T* __restrict__ qg, T* __restrict__ out, float* __restrict__ part_o,
+                   float* __restrict__ part_lse, float scale_log2, int32_t* __restrict__ sched) {
+  using L = Layout<D>;
+  using namespace sm100;
+  constexpr bool kSplit = Fmt<T>::kSplit;
+  constexpr int KB = L::KB;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sb = smem_u32(smem);
+  uint32_t* tmem_slot = (uint32_t*)(smem + L::kOffBar + 2 * BARS_PER_LANE * 8);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef PAT_TC_TRACE
+  const bool traced = (int)blockIdx.x == g_trace_cta;
+#endif
+  // lane (pipeline) of this warp: control warps 0,1 -> 0 and 2,3 -> 1; softmax 4-7 -> 0, 8-11 -> 1
+  const int pl = warp < 4 ? (warp >> 1) : ((warp - 4) >> 2);
+  const uint32_t bars = sb + L::kOffBar + (uint32_t)(pl * BARS_PER_LANE * 8);
+  auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
+  const uint32_t ring_kv = sb + L::kOffKV + (uint32_t)(pl * L::kLaneRing);
+  auto sK = [&](int s) { return ring_kv + (uint32_t)(s * 2 * L::kTileBytes); };
+  auto sV = [&](int s) { return ring_kv + (uint32_t)(s * 2 * L::kTileBytes + L::kTileBytes); };
+  const uint32_t ring_s = sb + L::kOffRing + (uint32_t)(pl * 2 * kSlotBytes);
+  ItemSlot* ring = reinterpret_cast<ItemSlot*>(smem + L::kOffRing) + pl * 2;
+  auto fld = [&](uint32_t n, uint32_t off) { return lds_s32(ring_s + (n & 1) * kSlotBytes + off); };
+
+  const int H = plan.H, G = plan.G, bs = plan.bs;
+  const int n_items = plan.n_items[var];
+  const Item* items = plan.items[var];
+
+  if (tid < 2) {
+    const uint32_t b0 = sb + L::kOffBar + (uint32_t)(tid * BARS_PER_LANE * 8);
+    auto ib = [&](int i) { return b0 + 8u * (uint32_t)i; };
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(ib(KV_FULL + s), 1);
+      mbar_init(ib(KV_EMPTY + s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(ib(S_FULL + b), 1);
+      mbar_init(ib(P_FULL + b), 4);
+      mbar_init(ib(SP_FREE + b), 1);
+    }
+    mbar_init(ib(O_EMPTY), 1);
+    mbar_init(ib(QT_FULL), 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(ib(ITEM_FULL + i), 32);
+      mbar_init(ib(ITEM_EMPTY + i), 1 + 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tg = tmem + (uint32_t)(pl * 256);  // this lane's TMEM columns
+
+  if (warp < 4) {
+    if ((warp & 1) == 0) {
+      // ------------------------------------------------------------ producer
+      if (elect_one()) {
+        tma_prefetch(&tmk);
+        tma_prefetch(&tmv);
+      }
+      uint32_t gt = 0;
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t slot = n & 1;
+        mbar_wait(bar(ITEM_EMPTY + slot), ((n >> 1) & 1) ^ 1);
+        // the first item of lane L of CTA b is item b + L * grid (no claim
+        // latency at kernel start), later ones come from the counter
+        int it = (int)blockIdx.x + pl * (int)gridDim.x;
+        if (n > 0 && lane == 0) it = atomicAdd(sched, 1) + 2 * (int)gridDim.x;
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= n_items) it = -1;
+        Item item{};
+        if (it >= 0) {
+          item = load_item(items + it);
+          for (int r = lane; r < item.nrows; r += 32) {
+            const int qi = (item.row0 + r) / G;
+            ring[slot].meta[r] =
+                make_int2(__ldg(plan.pack_q + item.qoff + qi), __ldg(plan.unit_slot + item.slot_off + qi));
+          }
+          if (lane == 0) ring[slot].item = item;
+          // warm L2 with the item's Q rows (the softmax warps load them into
+          // TMEM at the previous item's end): one bulk prefetch per query
+          const int i0 = item.row0 / G, i1 = (item.row0 + item.nrows - 1) / G;
+          for (int i = i0 + lane; i <= i1; i += 32) {
+            const int qid = __ldg(plan.pack_q + item.qoff + i);
+            const int a = max(i * G, item.row0), e = min((i + 1) * G, item.row0 + item.nrows);
+            bulk_prefetch_l2(qg + ((int64_t)qid * H + item.kvh * G + (a - i * G)) * D, (uint32_t)((e - a) * D * 2));
+          }
+        }
+        if (lane == 0) ring[slot].idx = it;
+        __syncwarp();
+        mbar_arrive(bar(ITEM_FULL + slot));
+        if (it < 0) break;
+        const int h = item.kvh, ntok = item.ntok;
+        const int32_t* blist = plan.pack_blk + item.blk;
+        const int ntiles = (ntok + kN - 1) / kN;
+        for (int j = 0; j < ntiles; ++j, ++gt) {
+          const int s = gt % kStages;
+          const int rem = ntok - j * kN;
+          const int ngrp = rem >= kN ? kN / 16 : (rem + 15) / 16;  // 16-token page slices
+          int my_blk = 0, my_off = 0;
+          if (lane < ngrp) {
+            const int tok = j * kN + lane * 16;
+            const int pg = bs == 16 ? (tok >> 4) : tok / bs;
+            my_blk = __ldg(blist + pg);
+            my_off = bs == 16 ? 0 : tok - pg * bs;
+          }
+          mbar_wait(bar(KV_EMPTY + s), ((gt / kStages) & 1) ^ 1);
+          if (pl == 0) TC_TRACE(0, 0, gt);
+          if (elect_one()) mbar_expect_tx(bar(KV_FULL + s), (uint32_t)(ngrp * KB * 2048 * 2));
+          __syncwarp();
+          for (int gr = 0; gr < ngrp; ++gr) {
+            const int blk = __shfl_sync(0xffffffffu, my_blk, gr);
+            const int off = __shfl_sync(0xffffffffu, my_off, gr);
+            if (elect_one()) {
+#pragma unroll
+              for (int kb = 0; kb < KB; ++kb) {
+                tma_load_4d(sK(s) + kb * (kN * 128) + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
+                tma_load_4d(sV(s) + kb * (kN * 128) + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+    } else {
+      // ------------------------------------------------------------ MMA issuer
+      // Per lane tile g (ring position, S/P buffer b = g & 1): QK(g) needs the
+      // stage, and PV(g-2) done (it read P[b], which QK(g) overwrites); QK runs
+      // one tile ahead of PV, so the softmax of tile g overlaps QK(g+1).
+      constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
+      constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
+      uint32_t gt = 0, qu = 0, ou = 0;
+      auto qk = [&](uint32_t g, bool first) {
+        const int s = (int)(g % kStages);
+        const uint32_t b = g & 1;
+        if (pl == 0) TC_TRACE(1, 2, g);
+        mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
+        if (pl == 0) TC_TRACE(1, 3, g);
+#ifndef PAT_TC4_NO_SPWAIT
+        mbar_wait(bar(SP_FREE + b), ((g >> 1) & 1) ^ 1);
+#endif
+        if (first) mbar_wait(bar(QT_FULL), qu++ & 1);
+        tc_fence_after();
+        if (pl == 0) TC_TRACE(1, 0, g);
+        if (elect_one()) {
+          const uint64_t k0 = umma_desc_sw128(sK(s), 16, 1024);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const int kb = k >> 2, kk = k & 3;
+            // Q(m, k) packed two per column: a k-step of 16 = 8 columns
+            umma_f16_ts(tg + 32u * b, tg + 64u + (uint32_t)(k * 8),
+                        k0 + (uint64_t)((kb * (kN * 128) + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
+          }
+          umma_commit(bar(S_FULL + b));
+        }
+        __syncwarp();
+      };
+      for (uint32_t n = 0;; ++n) {
+        mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1);
+        const int it = fld(n, kFIdx);
+        const int ntok = it >= 0 ? fld(n, kFNtok) : 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
+        if (it < 0) break;
+        const int ntiles = (ntok + kN - 1) / kN;
+        qk(gt, true);
+        for (int t = 0; t < ntiles; ++t) {
+          const uint32_t g = gt + (uint32_t)t, b = g & 1;
+          if (t + 1 < ntiles) qk(g + 1, false);
+          if (pl == 0) TC_TRACE(1, 4, g);
+          mbar_wait(bar(P_FULL + b), (g >> 1) & 1);
+          if (t == 0) mbar_wait(bar(O_EMPTY), (ou & 1) ^ 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const int s = (int)(g % kStages);
+            const uint64_t v0 = umma_desc_sw128(sV(s), kN * 128, 1024);
+#pragma unroll
+            for (int k = 0; k < kN / 16; ++k) {
+              const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
+              // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
+              umma_f16_ts(tg + 128u, tg + 32u * b + (uint32_t)(k * 8), bd, idesc_pv, (t == 0 && k == 0) ? 0u : 1u);
+              if constexpr (kSplit)
+                umma_f16_ts(tg + 128u, tg + 32u * b + 16u + (uint32_t)(k * 8), bd, idesc_pv, 1u);
+            }
+            umma_commit(bar(SP_FREE + b));
+            umma_commit(bar(KV_EMPTY + s));
+          }
+          __syncwarp();
+          if (pl == 0) TC_TRACE(1, 1, g);
+        }
+        ++ou;
+        gt += (uint32_t)ntiles;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue
+    const int wq = warp & 3;          // TMEM lane quarter
+    const int ln = wq * 32 + lane;    // TMEM lane = row of the item
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const uint32_t sp = tg + lane_base;
+#ifdef PAT_TC_TRACE
+    const bool tr = (wq == 0 && lane == 0);
+#endif
+    uint32_t gt = 0;
+
+    auto wait_item = [&](uint32_t n) { mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1); };
+    // this thread's Q row of item n (zeros past the item's rows) into registers
+    auto load_q = [&](uint32_t n, uint32_t* qv) {
+      const bool live = ln < fld(n, kFNrows);
+      const uint4* src = nullptr;
+      if (live) {
+        const int qid = fld(n, kFMeta + 8 * ln);
+        const int head = fld(n, kFKvh) * G + (fld(n, kFRow0) + ln) % G;
+        src = reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + head) * D);
+      }
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) {
+        const uint4 v = live ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+        qv[4 * i] = v.x, qv[4 * i + 1] = v.y, qv[4 * i + 2] = v.z, qv[4 * i + 3] = v.w;
+      }
+    };
+    auto store_q = [&](const uint32_t* qv, bool warp_live) {
+      if (warp_live) {
+#pragma unroll
+        for (int i = 0; i < D / 64; ++i) tmem_st32_nowait(sp + 64u + 32u * i, qv + 32 * i);
+        tmem_wait_st();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(QT_FULL));
+    };
+
+    wait_item(0);
+    if (fld(0, kFIdx) >= 0) {
+      uint32_t qv[D / 2];
+      const bool wl = wq * 32 < fld(0, kFNrows);
+      if (wl) load_q(0, qv);
+      store_q(qv, wl);
+    }
+    for (uint32_t n = 0;; ++n) {
+      if (fld(n, kFIdx) < 0) break;  // ITEM_FULL(n) already waited
+      const int ntok = fld(n, kFNtok);
+      const int nrows = fld(n, kFNrows);
+      const int kvh = fld(n, kFKvh), row0 = fld(n, kFRow0);
+      const int ntiles = (ntok + kN - 1) / kN;
+      const bool wlive = wq * 32 < nrows;  // warp has live rows (warp-uniform)
+      float m_ref = -INFINITY;             // running max, log2 units
+      float2 l2 = make_float2(0.f, 0.f);
+      bool have_next = false, next_live = false;
+      uint32_t qv[D / 2];
+      long long it0 = 0, it1 = 0, it2 = 0, it3 = 0;
+      (void)it0, (void)it1, (void)it2, (void)it3;
+#ifdef PAT_TC_TRACE
+      if (tr) ITEM_T(it0);
+#endif
+
+      for (int t = 0; t < ntiles; ++t) {
+        const uint32_t g = gt + (uint32_t)t, b = g & 1;
+        if (t == ntiles - 1) {
+          // next item: fetch its Q rows now (L2-warm: the producer prefetched
+          // them at claim time) so the loads overlap this last tile
+          wait_item(n + 1);
+          have_next = fld(n + 1, kFIdx) >= 0;
+          next_live = have_next && wq * 32 < fld(n + 1, kFNrows);
+          if (next_live) load_q(n + 1, qv);
+        }
+        mbar_wait(bar(S_FULL + b), (g >> 1) & 1);
+#ifdef PAT_TC_TRACE
+        if (tr && t == 0) ITEM_T(it1);
+        if (tr && pl == 0) TC_TRACE(2, 0, g);
+#endif
+        tc_fence_after();
+        const uint32_t spb = sp + 32u * b;
+        if (wlive) {
+          uint32_t sr[kN];
+          tmem_ld32(spb, sr);
+          const int valid = ntok - t * kN;
+          if (valid < kN) {
+#pragma unroll
+            for (int k = 0; k < kN; ++k)
+              if (k >= valid) sr[k] = __float_as_uint(-INFINITY);
+          }
+          float pm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int k = 0; k < kN / 8; ++k)
+            pm[k & 3] = fmax3(pm[k & 3],
+                              fmax3(__uint_as_float(sr[8 * k]), __uint_as_float(sr[8 * k + 1]),
+                                    __uint_as_float(sr[8 * k + 2])),
+                              fmax3(__uint_as_float(sr[8 * k + 3]), __uint_as_float(sr[8 * k + 4]),
+                                    fmax3(__uint_as_float(sr[8 * k + 5]), __uint_as_float(sr[8 * k + 6]),
+                                          __uint_as_float(sr[8 * k + 7]))));
+          const float mx = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])) * scale_log2;
+          const bool need = mx > m_ref + kRescaleThreshold;
+          if (__any_sync(0xffffffffu, need)) {
+            const float m_new = need ? mx : m_ref;
+            const float alpha = m_new == -INFINITY ? 1.f : ex2_approx(m_ref - m_new);
+            if (t > 0) {
+              // O must hold the previous tile's PV before it is rescaled
+              const uint32_t gp = g - 1;
+              mbar_wait(bar(SP_FREE + (gp & 1)), (gp >> 1) & 1);
+              tc_fence_after();
+#pragma unroll 1
+              for (int q = 0; q < D / 16; ++q) {
+                uint32_t o[16];
+                const uint32_t ta = sp + 128u + (uint32_t)(q * 16);
+                tmem_ld16(ta, o);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                tmem_st16_wait(ta, o);
+              }
+            }
+            l2.x *= alpha;
+            l2.y *= alpha;
+            m_ref = m_new;
+          }
+          // P = exp2(s * scale - m_ref), packed pairs (a row with no valid
+          // column so far keeps m_ref = -inf: reference 0, P = 0)
+          const float mu = m_ref == -INFINITY ? 0.f : m_ref;
+          const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mu, -mu);
+          uint32_t ph[kN / 2], plo[kN / 2];
+#pragma unroll
+          for (int k = 0; k < kN / 2; ++k) {
+            float2 a = __ffma2_rn(make_float2(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sc2, nm2);
+            a.x = ex2_approx(a.x);
+            a.y = ex2_approx(a.y);
+            ph[k] = Fmt<T>::pack(a.x, a.y);
+            if constexpr (kSplit) {
+              const float2 hf = Fmt<T>::unpack(ph[k]);
+              const float2 lo = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
+              plo[k] = Fmt<T>::pack(lo.x, lo.y);
+              l2 = __fadd2_rn(l2, a);
+            } else {
+              // normalise by the sum of the ROUNDED weights the MMA actually uses
+              l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
+            }
+          }
+          tmem_st_n<kN / 2>(spb, ph);
+          if constexpr (kSplit) tmem_st_n<kN / 2>(spb + 16u, plo);
+        }
+        if (t * kN + kN > ntok) {
+          // tail tile: zero V rows past the span (stale / uninitialised smem,
+          // P == 0 there must not meet a NaN)
+          const int vt = ntok - t * kN;
+          const int s = (int)(g % kStages);
+          const int nz = (kN - vt) * KB * 8;
+          for (int q = ln; q < nz; q += kM) {
+            const int rr = vt + q / (KB * 8);
+            const int kb = (q / 8) % KB, ch = q % 8;
+            st_shared_v4(sV(s) + kb * (kN * 128) + rr * 128 + (ch << 4), make_uint4(0, 0, 0, 0));
+          }
+          fence_proxy_async_smem();
+        }
+        if (wlive) tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(P_FULL + b));
+#ifdef PAT_TC_TRACE
+        if (tr && pl == 0) TC_TRACE(2, 1, g);
+#endif
+      }
+#ifdef PAT_TC_TRACE
+      if (tr) ITEM_T(it2);
+#endif
+      // The item's last QK completed (its S was consumed above): the next
+      // item's Q goes into TMEM now, so its first QK overlaps this epilogue.
+      if (have_next) store_q(qv, next_live);
+
+      // ---- epilogue: the last PV of the item done -> O / l of this row
+      const uint32_t gl = gt + (uint32_t)ntiles - 1;
+      mbar_wait(bar(SP_FREE + (gl & 1)), (gl >> 1) & 1);
+      tc_fence_after();
+      const bool live = ln < nrows;
+      const float l = l2.x + l2.y;
+      const int2 meta = live ? lds_v2(ring_s + (n & 1) * kSlotBytes + kFMeta + 8 * ln) : make_int2(0, -1);
+      const int head = kvh * G + (live ? (row0 + ln) % G : 0);
+      if (wlive) {
+        const float inv = 1.f / l;
+#pragma unroll 1
+        for (int q = 0; q < D / 32; ++q) {
+          uint32_t o[32];
+          tmem_ld32(sp + 128u + (uint32_t)(q * 32), o);
+          if (live) {
+            const float* f = reinterpret_cast<const float*>(o);
+            if (meta.y < 0) {
+              uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)meta.x * H + head) * D + q * 32);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                dst[k] = make_uint4(Fmt<T>::pack(f[8 * k] * inv, f[8 * k + 1] * inv),
+                                    Fmt<T>::pack(f[8 * k + 2] * inv, f[8 * k + 3] * inv),
+                                    Fmt<T>::pack(f[8 * k + 4] * inv, f[8 * k + 5] * inv),
+                                    Fmt<T>::pack(f[8 * k + 6] * inv, f[8 * k + 7] * inv));
+            } else {
+              float4* dst = reinterpret_cast<float4*>(part_o + ((int64_t)meta.y * H + head) * D + q * 32);
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                dst[k] = make_float4(f[4 * k] * inv, f[4 * k + 1] * inv, f[4 * k + 2] * inv, f[4 * k + 3] * inv);
+            }
+          }
+        }
+        if (live && meta.y >= 0) part_lse[(int64_t)meta.y * H + head] = m_ref + log2f(l);
+      }
+      // O read by the lane's four warps: the next item's first PV may overwrite it
+      tc_fence_before();
+      named_bar_sync(1 + pl, 128);
+      if (wq == 0 && lane == 0) mbar_arrive(bar(O_EMPTY));
+#ifdef PAT_TC_TRACE
+      if (tr) {
+        ITEM_T(it3);
+        const int k = atomicAdd(&g_item_n, 1);
+        if (k < kItemLog) {
+          long long* e = g_item_log[k];
+          e[0] = blockIdx.x * 2 + pl, e[1] = fld(n, kFIdx), e[2] = nrows, e[3] = ntiles;
+          e[4] = it0, e[5] = it1, e[6] = it2, e[7] = it3;
+        }
+      }
+#endif
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
+      gt += (uint32_t)ntiles;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+  if (tid == 0) {
+    // the last CTA out re-arms the item counter for the next launch
+    __threadfence();
+    if (atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace tc4
+
+template <int D, typename T>
+static cudaError_t launch_tc4_t(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var,
+                                int grid, const void* q, void* out, float* po, float* pl, float scale_log2,
+                                int32_t* sched, cudaStream_t st) {
+  constexpr int smem = tc4::Layout<D>::kAlloc;
+  // the opt-in is per device; setting it is cheap and idempotent
+  cudaError_t e = cudaFuncSetAttribute(tc4::fwd_tc4_kernel<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  tc4::fwd_tc4_kernel<D, T><<<grid, tc4::kThreads, smem, st>>>(tmk, tmv, plan, var, (const T*)q, (T*)out, po, pl,
+                                                               scale_log2, sched);
+  return cudaGetLastError();
+}
+
+#ifdef PAT_TC_TRACE
+extern "C" int pat_debug_tc_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, tc4::g_tc_trace, sizeof(tc4::g_tc_trace));
+}
+extern "C" int pat_debug_trace_cta(int cta) {
+  static long long zero[4][8][tc4::kTraceSteps];
+  cudaMemcpyToSymbol(tc4::g_tc_trace, zero, sizeof(zero));
+  return (int)cudaMemcpyToSymbol(tc4::g_trace_cta, &cta, sizeof(int));
+}
+extern "C" int pat_debug_item_log(long long* host, int* n) {
+  int e = (int)cudaMemcpyFromSymbol(n, tc4::g_item_n, sizeof(int));
+  if (e) return e;
+  e = (int)cudaMemcpyFromSymbol(host, tc4::g_item_log, sizeof(tc4::g_item_log));
+  int zero = 0;
+  cudaMemcpyToSymbol(tc4::g_item_n, &zero, sizeof(int));
+  return e;
+}
+extern "C" int pat_debug_spans_tc(unsigned long long* host) {
+  int e = (int)cudaMemcpyFromSymbol(host, tc4::g_span_tc, sizeof(tc4::g_span_tc));
+  static unsigned long long zero[1][kSpanCtas][2];
+  cudaMemcpyToSymbol(tc4::g_span_tc, zero, sizeof(zero));
+  return e;
+}
+#endif
+
+cudaError_t launch_forward_tc(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var, int grid,
+                              int dtype, int d, const void* q, void* out, float* po, float* pl, float scale_log2,
+                              int32_t* sched, cudaStream_t st) {
+  if (dtype == PAT_DTYPE_F16) {
+    if (d == 128) return launch_tc4_t<128, __half>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, sched, st);
+    return launch_tc4_t<64, __half>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, sched, st);
+  }
+  if (d == 128)
+    return launch_tc4_t<128, __nv_bfloat16>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, sched, st);
+  return launch_tc4_t<64, __nv_bfloat16>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, sched, st);
+}
+
+}  // namespace pat

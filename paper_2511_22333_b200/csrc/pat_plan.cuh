@@ -12,11 +12,11 @@ namespace pat {
 // Kernel variants: rows of a work item = (#queries x G) rounded to a row tile.
 //   V16 / V32 / V64: mma.sync m16n8k16 streaming kernel with 1 / 2 / 4 row tiles
 //   of 16 rows per CTA (4 warps; the warps of a row tile split the KV tile);
-//   TC: tcgen05 kernel, items of up to 256 rows (two 128-lane softmax groups).
+//   TC: tcgen05 kernel, items of up to 128 rows (one TMEM lane per row).
 enum Variant : int { VAR_R16 = 0, VAR_R32 = 1, VAR_R64 = 2, VAR_TC = 3, NUM_VARIANTS = 4 };
 
 PAT_HD int variant_rows(int v) {
-  return v == VAR_R16 ? 16 : (v == VAR_R32 ? 32 : (v == VAR_R64 ? 64 : 256));
+  return v == VAR_R16 ? 16 : (v == VAR_R32 ? 32 : (v == VAR_R64 ? 64 : 128));
 }
 // Packs with at least `tc_min_rows` rows go to the tensor-core kernel.
 PAT_HD int choose_variant(int rows, int tc_min_rows) {

@@ -10,13 +10,17 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <queue>
 
 #include "pat_plan_host.h"
 
 namespace pat {
 
-// Hand-tuned round-1 constants (see DESIGN.md §4.7 for the measured fits).
-static pat_cost_model g_cost_model = {3000.0, 0.0, 700.0, 1500.0, 6.0e3};
+// Measured on B200 for the two-lane tcgen05 kernel (tools/item_log.py: ~0.72 us
+// per 32-token tile per lane with every SM streaming, ~1.2 us + ~2 us per 128
+// rows of item boundary); see DESIGN.md §4.
+static pat_cost_model g_cost_model = {1200.0, 2000.0, 1440.0, 1500.0, 6.5e3};
+constexpr int kTcLanesPerSm = 2;  // independent item pipelines per tcgen05 CTA
 static std::mutex g_cost_mu;
 
 const pat_cost_model& cost_model() { return g_cost_model; }
@@ -42,11 +46,10 @@ void split_pack(int npages, int kv, int bs, int parts, std::vector<Part>& out) {
 
 
 // Estimated time (ns) of one work item of variant v with `rows` rows over
-// `ntok` tokens, measured on B200 (tools/tc_trace.py): the tcgen05 kernel runs
-// a 64-token KV tile of up to 128 rows in ~0.7 us (softmax-chain bound, about
-// one SM's HBM share of 32 KB when all SMs stream) plus ~3 us per item (next
-// item's KV and Q latency, epilogue); the mma.sync streaming kernel is
-// HBM-paced.
+// `ntok` tokens, measured on B200: a tcgen05 lane streams a 64-token span of up
+// to 128 rows in ~1.4 us when every SM streams (two lanes per SM share the
+// chip's ~7 TB/s L2 -> SM bandwidth) plus the item boundary (Q load, last PV,
+// epilogue stores); the mma.sync streaming kernel is HBM-paced.
 double item_ns(const ScheduleParams& sp, int v, int rows, int ntok) {
   const pat_cost_model& cm = cost_model();
   const double steps = (double)ceil_div(ntok, 64);
@@ -54,6 +57,22 @@ double item_ns(const ScheduleParams& sp, int v, int rows, int ntok) {
   if (v == VAR_TC)
     return cm.tc_item_ns + cm.tc_item_row_ns * rows / 128.0 + steps * cm.tc_step_ns * (0.5 + 0.5 * dscale);
   return cm.stream_item_ns + steps * 64.0 * sp.d * 4 / (cm.hbm_bytes_per_ns / std::max(sp.num_sms, 1));
+}
+
+// Makespan of greedy longest-first list scheduling of `costs` over `lanes`
+// identical workers -- what the tcgen05 kernel's dynamic claims do.
+double lpt_makespan(std::vector<double>& costs, int lanes) {
+  std::sort(costs.begin(), costs.end(), std::greater<double>());
+  std::priority_queue<double, std::vector<double>, std::greater<double>> free_at;
+  for (int i = 0; i < lanes; ++i) free_at.push(0.0);
+  double mk = 0;
+  for (double c : costs) {
+    double t = free_at.top() + c;
+    free_at.pop();
+    free_at.push(t);
+    mk = std::max(mk, t);
+  }
+  return mk;
 }
 
 // Native KV split for B200.  Picks one chunk size (pages) for all packs by
@@ -77,23 +96,34 @@ void native_parts(const HostPacks& P, const ScheduleParams& sp, std::vector<int>
   }
   std::vector<std::pair<int, double>> cand;
   std::vector<double> worsts;
+  int64_t total_row_blocks_pages = 0;
+  for (int p = 0; p < NP; ++p)
+    total_row_blocks_pages += (int64_t)pages[p] * ceil_div(rows[p], variant_rows(choose_variant(rows[p], sp.tc_min_rows)));
+  const int64_t max_items = (int64_t)64 * kTcLanesPerSm * std::max(sp.num_sms, 1);
+  std::vector<double> tc_costs;
   for (int chunk = 1;; chunk *= 2) {
     const int c = std::min(chunk, maxpages);
+    // far more items than lanes can balance only costs item boundaries
+    if (c < maxpages && total_row_blocks_pages * sp.KVH / c > max_items) continue;
     double work = 0, worst = 0, extra = 0;
     double vwork[NUM_VARIANTS] = {0, 0, 0, 0};
     int64_t vitems[NUM_VARIANTS] = {0, 0, 0, 0};
+    tc_costs.clear();
     for (int p = 0; p < NP; ++p) {
       const int parts = (int)ceil_div(pages[p], c);
       const int v = choose_variant(rows[p], sp.tc_min_rows);
       const int R = variant_rows(v);
-      const int ntok = std::min(c, pages[p]) * sp.bs;
       for (int r0 = 0; r0 < rows[p]; r0 += R) {
-        const double item = item_ns(sp, v, std::min(R, rows[p] - r0), ntok);
+        // near-equal parts (split_pack): the larger ones carry ceil(pages / parts)
+        const int big = (int)ceil_div(pages[p], parts);
+        const double item = item_ns(sp, v, std::min(R, rows[p] - r0), std::min(big * sp.bs, P.kv[p]));
         const int64_t n = (int64_t)parts * sp.KVH;
         vitems[v] += n;
         vwork[v] += item * n;
         work += item * n;
         worst = std::max(worst, item);
+        if (v == VAR_TC)
+          for (int64_t i = 0; i < n; ++i) tc_costs.push_back(item);
       }
       if (parts > 1) extra += (double)parts * (P.q_off[p + 1] - P.q_off[p]) * sp.H * sp.d * 8;
     }
@@ -103,24 +133,25 @@ void native_parts(const HostPacks& P, const ScheduleParams& sp, std::vector<int>
       if (!vitems[v]) continue;
       const int sms = std::max(1, (int)(sp.num_sms * vwork[v] / work + 0.5));
       const double mean = vwork[v] / vitems[v];
-      if (v == VAR_TC)  // dynamic longest-first: average load plus half a mean item of tail
-        tv = std::max(tv, vwork[v] / sms + 0.5 * mean);
+      if (v == VAR_TC)  // dynamic longest-first claims over the kernel's lanes
+        tv = std::max(tv, lpt_makespan(tc_costs, sms * kTcLanesPerSm));
       else
         tv = std::max(tv, (double)ceil_div(vitems[v], sms) * mean);
     }
-    const double est = std::max({(kv_bytes + extra) / bw, tv, worst});
+    const double est = std::max({(kv_bytes + extra) / bw, tv, vitems[VAR_TC] ? 0.0 : worst});
     cand.emplace_back(c, est);
-    worsts.push_back(worst);
+    worsts.push_back(vitems[VAR_TC] ? 0.0 : worst);
     if (getenv("PAT_DEBUG_SPLIT")) fprintf(stderr, "chunk %d bytes %.1f tv %.1f worst %.1f est %.1f\n", c, (kv_bytes + extra) / bw / 1e3, tv / 1e3, worst / 1e3, est / 1e3);
     if (c >= maxpages) break;
   }
   double best = 1e300;
   for (auto& ce : cand) best = std::min(best, ce.second);
-  // the largest chunk within 3% of the best estimate (fewest splits) whose
-  // longest item stays under half the makespan (robust to cost-model error)
+  // the largest chunk within 2% of the best estimate (fewest splits) whose
+  // longest item stays under half the makespan (robust to cost-model error;
+  // the tcgen05 estimate simulates the claims, so its tail is already in it)
   int best_chunk = 0;
   for (size_t i = 0; i < cand.size(); ++i)
-    if (cand[i].second <= best * 1.03 && worsts[i] <= 0.5 * cand[i].second)
+    if (cand[i].second <= best * 1.02 && worsts[i] <= 0.5 * cand[i].second)
       best_chunk = std::max(best_chunk, cand[i].first);
   if (best_chunk <= 0)
     for (auto& ce : cand)

@@ -33,10 +33,10 @@ def _units(name):
         plan.close()
 
 
-def test_default_model_is_the_round1_constants():
+def test_default_model_is_the_measured_two_lane_constants():
     m = CAL.get_cost_model()
     assert (m.tc_item_ns, m.tc_item_row_ns, m.tc_step_ns, m.stream_item_ns, m.hbm_bytes_per_ns) == \
-        (3000.0, 0.0, 700.0, 1500.0, 6000.0)
+        (1200.0, 2000.0, 1440.0, 1500.0, 6500.0)
 
 
 def test_set_get_roundtrip_and_validation(restore_model):

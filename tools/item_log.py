@@ -67,10 +67,11 @@ def run(name, tc_min_rows=0):
             idle[c] = (end - e[m, 7].max()) / 1e3
             first[c] = (e[m, 4].min() - t0) / 1e3
     tot = span * ncta
-    print(f"   per CTA avg: start-lat {start_lat.sum() / ncta:.1f}  tiles {tiles.sum() / ncta:.1f}  "
+    print(f"   per lane (CTA x pipeline, {ncta}) avg: start-lat {start_lat.sum() / ncta:.1f}  tiles {tiles.sum() / ncta:.1f}  "
           f"epilogue {epi.sum() / ncta:.1f}  idle-tail {idle.mean():.1f}  late-start {first.mean():.1f}  us "
           f"(of {span:.1f})")
-    kinds = {"ns(<=16)": e[:, 2] <= 16, "eo(17-128)": (e[:, 2] > 16) & (e[:, 2] <= 128), "pp(>128)": e[:, 2] > 128}
+    kinds = {"<=16": e[:, 2] <= 16, "17-64": (e[:, 2] > 16) & (e[:, 2] <= 64), "65-128": (e[:, 2] > 64) & (e[:, 2] <= 128),
+             ">128": e[:, 2] > 128}
     for k, m in kinds.items():
         if not m.any():
             continue

@@ -89,13 +89,11 @@ def main():
     lib.pat_debug_tc_trace.argtypes = [C.c_void_p]
     assert lib.pat_debug_tc_trace(tr.ctypes.data) == 0
     t0 = tr[0, 0, 0]
-    names = {(0, 0): "prod_kvempty", (1, 5): "mma_item_q", (1, 0): "mma_kvfull", (1, 1): "mma_qk_issued",
-             (1, 4): "mma_pv_start", (1, 2): "mma_pv_issued",
-             (2, 0): "sm_sfull", (2, 6): "sm_sloaded", (2, 7): "sm_maxed", (2, 1): "sm_exp_done",
-             (2, 3): "sm_pfull", (3, 1): "epi_pvdone", (3, 2): "epi_done"}
+    names = {(0, 0): "prod_tma", (1, 2): "mma_wait_kv", (1, 3): "mma_kv_ok", (1, 0): "mma_qk",
+             (1, 4): "mma_wait_p", (1, 1): "mma_pv", (2, 0): "sm_sfull", (2, 1): "sm_pfull"}
     hdr = " step " + " ".join(f"{v:>15s}" for v in names.values())
     print(hdr)
-    n = min(args.steps, ntok // 64) if ntok else args.steps
+    n = min(args.steps, ntok // 32) if ntok else args.steps
     for s in range(n):
         row = []
         for (r, e) in names:
@@ -103,7 +101,7 @@ def main():
             row.append(f"{(v - t0) if v else -1:>15d}")
         print(f"{s:5d} " + " ".join(row))
     # steady-state per-step cycles from the MMA issuer's KV_FULL timestamps
-    m = tr[1, 0, :n]
+    m = tr[1, 3, :n]
     m = m[m > 0]
     if len(m) > 4:
         d = np.diff(m[2:])
