@@ -55,8 +55,15 @@ def pat_attention(plan: PatPlan, q: torch.Tensor, k_cache: torch.Tensor, v_cache
         raise ShapeMismatch("tensors must be on a CUDA device")
     if not (q.is_contiguous() and k_cache.is_contiguous() and v_cache.is_contiguous()):
         raise ShapeMismatch("tensors must be contiguous")
+    # the kernels index q / out by the plan's query ids and map the caches with its page size
+    if q.shape[0] != plan.num_queries:
+        raise ShapeMismatch(f"Q row count must match the table: {q.shape[0]} != {plan.num_queries}")
+    if k_cache.shape[1] != plan.block_size:
+        raise ShapeMismatch(f"cache page size {k_cache.shape[1]} != plan block_size {plan.block_size}")
     if out is None:
         out = torch.empty_like(q)
+    elif out.shape != q.shape or out.dtype != q.dtype or out.device != q.device or not out.is_contiguous():
+        raise ShapeMismatch("out must be a contiguous tensor with q's shape, dtype and device")
     need = plan.workspace_bytes()
     if workspace is None or workspace.numel() * workspace.element_size() < need:
         workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=q.device)
@@ -143,6 +150,9 @@ class PatDecoder:
 
     def forward_device(self, block_tables, seq_lens, q, k_cache, v_cache, out=None, scale=None):
         """Decode attention straight from vLLM-style device block tables."""
+        if block_tables.dim() != 2 or block_tables.shape[0] != q.shape[0] or seq_lens.shape[0] != q.shape[0]:
+            raise ShapeMismatch(f"Q row count must match the table: q {tuple(q.shape)}, block_tables "
+                                f"{tuple(block_tables.shape)}, seq_lens {tuple(seq_lens.shape)}")
         plan = self.plan_for_device(block_tables, seq_lens, k_cache.shape[1])
         return pat_attention(plan, q, k_cache, v_cache, out=out, workspace=self.workspace(plan), scale=scale)
 

@@ -178,6 +178,7 @@ int upload(pat_plan* P) {
     P->items_cap[v] = nit[v];
   }
   size_t o_nit = b.add(nit, sizeof(nit));
+  size_t o_npr = b.add(s.n_pair, sizeof(s.n_pair));
   size_t o_mq = b.addv(s.merge_q), o_qso = b.addv(s.q_slot_off), o_qn = b.addv(s.q_nslot);
   std::vector<int32_t> mdesc;
   for (int32_t q : s.merge_q) mdesc.insert(mdesc.end(), {q, s.q_slot_off[q], s.q_nslot[q], 0});
@@ -202,6 +203,7 @@ int upload(pat_plan* P) {
   D.unit_slot = (const int32_t*)(base + o_us);
   for (int v = 0; v < NUM_VARIANTS; ++v) D.items[v] = (const Item*)(base + o_it[v]);
   D.n_items = (const int32_t*)(base + o_nit);
+  D.n_pair = (const int32_t*)(base + o_npr);
   D.merge_q = (const int32_t*)(base + o_mq);
   D.merge_desc = (const int4*)(base + o_md);
   D.q_slot_off = (const int32_t*)(base + o_qso);
@@ -230,6 +232,7 @@ int finish_plan(pat_plan* P, const RowsView& R, int flags) {
     P->tc_min_rows = max_rows <= 16 ? 0 : 1;
   }
   ScheduleParams sp{P->B, P->bs, P->H, P->KVH, P->d, P->split_mode, P->num_sms, P->tc_min_rows};
+  sp.pair_items = (flags & PAT_PLAN_PAIR_ITEMS) != 0;
   int st = host_schedule(P->packs, sp, &P->sched);
   if (st) return st;
   P->n_slots = P->sched.n_slots;

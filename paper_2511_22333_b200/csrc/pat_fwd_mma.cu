@@ -530,13 +530,9 @@ static cudaError_t launch_fwd_t(const CUtensorMap& tmk, const CUtensorMap& tmv, 
                                 int grid, const void* q, void* out, float* po, float* pl, float scale_log2,
                                 cudaStream_t st) {
   constexpr int smem = StreamSmem<WM, D>::kAlloc;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e =
-        cudaFuncSetAttribute(fwd_stream_kernel<WM, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
+  // the opt-in is per device; setting it on every launch is cheap and idempotent
+  cudaError_t e = cudaFuncSetAttribute(fwd_stream_kernel<WM, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
   fwd_stream_kernel<WM, D, T><<<grid, kStreamThreads, smem, st>>>(tmk, tmv, plan, var, (const T*)q, (T*)out, po,
                                                                   pl, scale_log2);
   return cudaGetLastError();

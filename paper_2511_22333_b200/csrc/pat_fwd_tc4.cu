@@ -87,13 +87,13 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 struct ItemSlot {
   int32_t idx;
-  int32_t pad[7];
+  int32_t pad[7];  // [0] joined pair item (tiles from lane 0's ring), [1] its first ring position
   Item item;
   int2 meta[kM];  // (qid, slot) per row
 };
 static_assert(sizeof(ItemSlot) == 64 + 8 * kM, "ItemSlot layout");
 constexpr uint32_t kSlotBytes = sizeof(ItemSlot);
-constexpr uint32_t kFIdx = 0, kFKvh = 32 + 4, kFRow0 = 32 + 8, kFNrows = 32 + 12, kFNtok = 32 + 20, kFMeta = 64;
+constexpr uint32_t kFIdx = 0, kFShared = 4, kFG0 = 8, kFKvh = 32 + 4, kFRow0 = 32 + 8, kFNrows = 32 + 12, kFNtok = 32 + 20, kFMeta = 64;
 
 template <int D>
 struct Layout {
@@ -118,9 +118,12 @@ enum Bar : int {
   QT_FULL = O_EMPTY + 1,        // the item's Q rows stored in TMEM (4 warps)
   ITEM_FULL = QT_FULL + 1,      // [slot] published by the producer (32 lanes)
   ITEM_EMPTY = ITEM_FULL + 2,   // [slot] released by the MMA warp and the 4 softmax warps
-  BARS_PER_LANE = ITEM_EMPTY + 2
+  XKV_EMPTY = ITEM_EMPTY + 2,   // [stage] lane 0 only: lane 1 released a pair tile of lane 0's ring
+  JOIN_FULL = XKV_EMPTY + kStages,  // [2] lane 0 only: join mailbox entry posted
+  JOIN_EMPTY = JOIN_FULL + 2,       // [2] lane 0 only: join mailbox entry read by lane 1
+  BARS_PER_LANE = JOIN_EMPTY + 2
 };
-static_assert(2 * BARS_PER_LANE * 8 + 8 <= 1024, "barrier area");
+static_assert(2 * BARS_PER_LANE * 8 + 32 <= 1024, "barrier area");
 
 template <typename T> struct Fmt;
 template <> struct Fmt<__half> {
@@ -205,11 +208,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   // lane (pipeline) of this warp: control warps 0,1 -> 0 and 2,3 -> 1; softmax 4-7 -> 0, 8-11 -> 1
   const int pl = warp < 4 ? (warp >> 1) : ((warp - 4) >> 2);
-  const uint32_t bars = sb + L::kOffBar + (uint32_t)(pl * BARS_PER_LANE * 8);
-  auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
-  const uint32_t ring_kv = sb + L::kOffKV + (uint32_t)(pl * L::kLaneRing);
-  auto sK = [&](int s) { return ring_kv + (uint32_t)(s * 2 * L::kTileBytes); };
-  auto sV = [&](int s) { return ring_kv + (uint32_t)(s * 2 * L::kTileBytes + L::kTileBytes); };
+  auto barL = [&](int l, int i) { return sb + L::kOffBar + (uint32_t)((l * BARS_PER_LANE + i) * 8); };
+  auto bar = [&](int i) { return barL(pl, i); };
+  // stage s of lane l's KV ring
+  auto sK = [&](int l, int s) { return sb + L::kOffKV + (uint32_t)(l * L::kLaneRing + s * 2 * L::kTileBytes); };
+  auto sV = [&](int l, int s) { return sK(l, s) + (uint32_t)L::kTileBytes; };
+  int2* join = reinterpret_cast<int2*>(smem + L::kOffBar + 2 * BARS_PER_LANE * 8 + 16);  // [2] mailbox
   const uint32_t ring_s = sb + L::kOffRing + (uint32_t)(pl * 2 * kSlotBytes);
   ItemSlot* ring = reinterpret_cast<ItemSlot*>(smem + L::kOffRing) + pl * 2;
   auto fld = [&](uint32_t n, uint32_t off) { return lds_s32(ring_s + (n & 1) * kSlotBytes + off); };
@@ -235,7 +239,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(ib(ITEM_FULL + i), 32);
       mbar_init(ib(ITEM_EMPTY + i), 1 + 4);
+      mbar_init(ib(JOIN_FULL + i), 1);
+      mbar_init(ib(JOIN_EMPTY + i), 1);
     }
+    for (int s = 0; s < kStages; ++s) mbar_init(ib(XKV_EMPTY + s), 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(smem_u32(tmem_slot));
@@ -252,19 +259,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch(&tmk);
         tma_prefetch(&tmv);
       }
-      uint32_t gt = 0;
+      // Phase 1 (pair items, > 128 rows): lane 0 claims them, posts each to the
+      // CTA's join mailbox with the ring position of its first tile and
+      // streams its tiles once; lane 1 takes rows 128.. of the same item and
+      // reads lane 0's ring (each stage is released by both lanes).  A "done"
+      // entry ends phase 1; then both lanes claim the other items
+      // independently.
+      const int n_pair = plan.n_pair[var];
+      bool pair_phase = n_pair > 0;
+      uint32_t gt = 0, jn = 0, pair_upto = 0;
       for (uint32_t n = 0;; ++n) {
         const uint32_t slot = n & 1;
         mbar_wait(bar(ITEM_EMPTY + slot), ((n >> 1) & 1) ^ 1);
-        // the first item of lane L of CTA b is item b + L * grid (no claim
-        // latency at kernel start), later ones come from the counter
-        int it = (int)blockIdx.x + pl * (int)gridDim.x;
-        if (n > 0 && lane == 0) it = atomicAdd(sched, 1) + 2 * (int)gridDim.x;
-        it = __shfl_sync(0xffffffffu, it, 0);
-        if (it >= n_items) it = -1;
+        int it = -1, shared = 0;
+        uint32_t g0 = 0;
+        if (pair_phase) {
+          if (pl == 0) {
+            int c = 0;
+            if (lane == 0) c = atomicAdd(sched + 0, 1);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            if (c < n_pair) it = c;
+            else pair_phase = false;
+            mbar_wait(barL(0, JOIN_EMPTY + (jn & 1)), ((jn >> 1) & 1) ^ 1);
+            if (lane == 0) {
+              join[jn & 1] = make_int2(it, (int)gt);
+              mbar_arrive(barL(0, JOIN_FULL + (jn & 1)));
+            }
+            __syncwarp();
+          } else {
+            mbar_wait(barL(0, JOIN_FULL + (jn & 1)), (jn >> 1) & 1);
+            const int2 e = lds_v2(smem_u32(&join[jn & 1]));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(barL(0, JOIN_EMPTY + (jn & 1)));
+            if (e.x >= 0) it = e.x, shared = 1, g0 = (uint32_t)e.y;
+            else pair_phase = false;
+          }
+          ++jn;
+        }
+        if (!pair_phase) {
+          int c = 0;
+          if (lane == 0) c = atomicAdd(sched + 2, 1);
+          it = n_pair + __shfl_sync(0xffffffffu, c, 0);
+          if (it >= n_items) it = -1;
+        }
         Item item{};
         if (it >= 0) {
           item = load_item(items + it);
+          if (it < n_pair) {  // pair item: lane 0 rows [0, 128), lane 1 the rest
+            if (pl == 0) item.nrows = kM;
+            else item.row0 += kM, item.nrows -= kM;
+          }
           for (int r = lane; r < item.nrows; r += 32) {
             const int qi = (item.row0 + r) / G;
             ring[slot].meta[r] =
@@ -280,13 +324,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_prefetch_l2(qg + ((int64_t)qid * H + item.kvh * G + (a - i * G)) * D, (uint32_t)((e - a) * D * 2));
           }
         }
-        if (lane == 0) ring[slot].idx = it;
+        if (lane == 0) {
+          ring[slot].idx = it;
+          ring[slot].pad[0] = shared;
+          ring[slot].pad[1] = (int)g0;
+        }
         __syncwarp();
         mbar_arrive(bar(ITEM_FULL + slot));
         if (it < 0) break;
+        if (shared) continue;  // the tiles come through lane 0's ring
         const int h = item.kvh, ntok = item.ntok;
         const int32_t* blist = plan.pack_blk + item.blk;
         const int ntiles = (ntok + kN - 1) / kN;
+        if (it < n_pair) pair_upto = gt + (uint32_t)ntiles;
         for (int j = 0; j < ntiles; ++j, ++gt) {
           const int s = gt % kStages;
           const int rem = ntok - j * kN;
@@ -299,6 +349,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             my_off = bs == 16 ? 0 : tok - pg * bs;
           }
           mbar_wait(bar(KV_EMPTY + s), ((gt / kStages) & 1) ^ 1);
+          // the previous occupant of this stage was a pair tile: lane 1 read it
+          // too (pair tiles are a prefix of lane 0's ring, so every earlier use
+          // of the stage was one: same parity as KV_EMPTY)
+          if (gt >= (uint32_t)kStages && gt - kStages < pair_upto)
+            mbar_wait(bar(XKV_EMPTY + s), ((gt / kStages) & 1) ^ 1);
           if (pl == 0) TC_TRACE(0, 0, gt);
           if (elect_one()) mbar_expect_tx(bar(KV_FULL + s), (uint32_t)(ngrp * KB * 2048 * 2));
           __syncwarp();
@@ -308,8 +363,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (elect_one()) {
 #pragma unroll
               for (int kb = 0; kb < KB; ++kb) {
-                tma_load_4d(sK(s) + kb * (kN * 128) + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
-                tma_load_4d(sV(s) + kb * (kN * 128) + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
+                tma_load_4d(sK(pl, s) + kb * (kN * 128) + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
+                tma_load_4d(sV(pl, s) + kb * (kN * 128) + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
               }
             }
             __syncwarp();
@@ -318,56 +373,58 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else {
       // ------------------------------------------------------------ MMA issuer
-      // Per lane tile g (ring position, S/P buffer b = g & 1): QK(g) needs the
-      // stage, and PV(g-2) done (it read P[b], which QK(g) overwrites); QK runs
-      // one tile ahead of PV, so the softmax of tile g overlaps QK(g+1).
+      // Per lane tile c (S/P buffer b = c & 1): QK(c) needs its KV stage and
+      // PV(c-2) done (it read P[b], which QK(c) overwrites); QK runs one tile
+      // ahead of PV, so the softmax of tile c overlaps QK(c+1).  The stage of
+      // tile t of an item is ring position base + t of the lane's own ring, or
+      // of lane 0's ring for a joined pair item.
       constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
       constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
-      uint32_t gt = 0, qu = 0, ou = 0;
-      auto qk = [&](uint32_t g, bool first) {
-        const int s = (int)(g % kStages);
-        const uint32_t b = g & 1;
-        if (pl == 0) TC_TRACE(1, 2, g);
-        mbar_wait(bar(KV_FULL + s), (g / kStages) & 1);
-        if (pl == 0) TC_TRACE(1, 3, g);
-#ifndef PAT_TC4_NO_SPWAIT
-        mbar_wait(bar(SP_FREE + b), ((g >> 1) & 1) ^ 1);
-#endif
-        if (first) mbar_wait(bar(QT_FULL), qu++ & 1);
-        tc_fence_after();
-        if (pl == 0) TC_TRACE(1, 0, g);
-        if (elect_one()) {
-          const uint64_t k0 = umma_desc_sw128(sK(s), 16, 1024);
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const int kb = k >> 2, kk = k & 3;
-            // Q(m, k) packed two per column: a k-step of 16 = 8 columns
-            umma_f16_ts(tg + 32u * b, tg + 64u + (uint32_t)(k * 8),
-                        k0 + (uint64_t)((kb * (kN * 128) + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
-          }
-          umma_commit(bar(S_FULL + b));
-        }
-        __syncwarp();
-      };
+      uint32_t tcnt = 0, rpos = 0, qu = 0, ou = 0;
       for (uint32_t n = 0;; ++n) {
         mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1);
         const int it = fld(n, kFIdx);
         const int ntok = it >= 0 ? fld(n, kFNtok) : 0;
+        const int src = it >= 0 && fld(n, kFShared) ? 0 : pl;  // ring the tiles come from
+        const uint32_t base = src != pl ? (uint32_t)fld(n, kFG0) : rpos;
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
         if (it < 0) break;
         const int ntiles = (ntok + kN - 1) / kN;
-        qk(gt, true);
+        auto qk = [&](int t, bool first) {
+          const uint32_t g = base + (uint32_t)t, c = tcnt + (uint32_t)t, b = c & 1;
+          const int s = (int)(g % kStages);
+          if (pl == 0) TC_TRACE(1, 2, c);
+          mbar_wait(barL(src, KV_FULL + s), (g / kStages) & 1);
+          if (pl == 0) TC_TRACE(1, 3, c);
+          mbar_wait(bar(SP_FREE + b), ((c >> 1) & 1) ^ 1);
+          if (first) mbar_wait(bar(QT_FULL), qu++ & 1);
+          tc_fence_after();
+          if (pl == 0) TC_TRACE(1, 0, c);
+          if (elect_one()) {
+            const uint64_t k0 = umma_desc_sw128(sK(src, s), 16, 1024);
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+              const int kb = k >> 2, kk = k & 3;
+              // Q(m, k) packed two per column: a k-step of 16 = 8 columns
+              umma_f16_ts(tg + 32u * b, tg + 64u + (uint32_t)(k * 8),
+                          k0 + (uint64_t)((kb * (kN * 128) + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
+            }
+            umma_commit(bar(S_FULL + b));
+          }
+          __syncwarp();
+        };
+        qk(0, true);
         for (int t = 0; t < ntiles; ++t) {
-          const uint32_t g = gt + (uint32_t)t, b = g & 1;
-          if (t + 1 < ntiles) qk(g + 1, false);
-          if (pl == 0) TC_TRACE(1, 4, g);
-          mbar_wait(bar(P_FULL + b), (g >> 1) & 1);
+          const uint32_t g = base + (uint32_t)t, c = tcnt + (uint32_t)t, b = c & 1;
+          if (t + 1 < ntiles) qk(t + 1, false);
+          if (pl == 0) TC_TRACE(1, 4, c);
+          mbar_wait(bar(P_FULL + b), (c >> 1) & 1);
           if (t == 0) mbar_wait(bar(O_EMPTY), (ou & 1) ^ 1);
           tc_fence_after();
           if (elect_one()) {
             const int s = (int)(g % kStages);
-            const uint64_t v0 = umma_desc_sw128(sV(s), kN * 128, 1024);
+            const uint64_t v0 = umma_desc_sw128(sV(src, s), kN * 128, 1024);
 #pragma unroll
             for (int k = 0; k < kN / 16; ++k) {
               const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
@@ -377,13 +434,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_f16_ts(tg + 128u, tg + 32u * b + 16u + (uint32_t)(k * 8), bd, idesc_pv, 1u);
             }
             umma_commit(bar(SP_FREE + b));
-            umma_commit(bar(KV_EMPTY + s));
+            umma_commit(src != pl ? barL(0, XKV_EMPTY + s) : bar(KV_EMPTY + s));
           }
           __syncwarp();
-          if (pl == 0) TC_TRACE(1, 1, g);
+          if (pl == 0) TC_TRACE(1, 1, c);
         }
         ++ou;
-        gt += (uint32_t)ntiles;
+        tcnt += (uint32_t)ntiles;
+        if (src == pl) rpos += (uint32_t)ntiles;
       }
     }
   } else {
@@ -395,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef PAT_TC_TRACE
     const bool tr = (wq == 0 && lane == 0);
 #endif
-    uint32_t gt = 0;
+    uint32_t tcnt = 0, rpos = 0;  // tiles consumed (S/P phases), own ring position
 
     auto wait_item = [&](uint32_t n) { mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1); };
     // this thread's Q row of item n (zeros past the item's rows) into registers
@@ -435,6 +493,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (fld(n, kFIdx) < 0) break;  // ITEM_FULL(n) already waited
       const int ntok = fld(n, kFNtok);
       const int nrows = fld(n, kFNrows);
+      const int src = fld(n, kFShared) ? 0 : pl;  // ring the item's tiles come from
+      const uint32_t base = src != pl ? (uint32_t)fld(n, kFG0) : rpos;
       const int kvh = fld(n, kFKvh), row0 = fld(n, kFRow0);
       const int ntiles = (ntok + kN - 1) / kN;
       const bool wlive = wq * 32 < nrows;  // warp has live rows (warp-uniform)
@@ -449,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 
       for (int t = 0; t < ntiles; ++t) {
-        const uint32_t g = gt + (uint32_t)t, b = g & 1;
+        const uint32_t g = tcnt + (uint32_t)t, b = g & 1;
         if (t == ntiles - 1) {
           // next item: fetch its Q rows now (L2-warm: the producer prefetched
           // them at claim time) so the loads overlap this last tile
@@ -535,12 +595,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           // tail tile: zero V rows past the span (stale / uninitialised smem,
           // P == 0 there must not meet a NaN)
           const int vt = ntok - t * kN;
-          const int s = (int)(g % kStages);
+          const int s = (int)((base + (uint32_t)t) % kStages);
           const int nz = (kN - vt) * KB * 8;
           for (int q = ln; q < nz; q += kM) {
             const int rr = vt + q / (KB * 8);
             const int kb = (q / 8) % KB, ch = q % 8;
-            st_shared_v4(sV(s) + kb * (kN * 128) + rr * 128 + (ch << 4), make_uint4(0, 0, 0, 0));
+            st_shared_v4(sV(src, s) + kb * (kN * 128) + rr * 128 + (ch << 4), make_uint4(0, 0, 0, 0));
           }
           fence_proxy_async_smem();
         }
@@ -560,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (have_next) store_q(qv, next_live);
 
       // ---- epilogue: the last PV of the item done -> O / l of this row
-      const uint32_t gl = gt + (uint32_t)ntiles - 1;
+      const uint32_t gl = tcnt + (uint32_t)ntiles - 1;
       mbar_wait(bar(SP_FREE + (gl & 1)), (gl >> 1) & 1);
       tc_fence_after();
       const bool live = ln < nrows;
@@ -610,7 +670,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
-      gt += (uint32_t)ntiles;
+      tcnt += (uint32_t)ntiles;
+      if (src == pl) rpos += (uint32_t)ntiles;
     }
   }
   tc_fence_before();
@@ -625,6 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
       sched[0] = 0;
       sched[1] = 0;
+      sched[2] = 0;
       __threadfence();
     }
   }

@@ -1,7 +1,7 @@
 // Merge of per-unit partials (o / l, log2-sum-exp) into the output: one warp
 // per (query, head), online-softmax fold in slot (= unit) order
-// (_merge_batch_into, attention.py:187-199).  Shared by the standalone merge
-// kernel and the tcgen05 kernel's fused merge phase.
+// (_merge_batch_into, attention.py:187-199).  Queries covered by one unit are
+// written by the forward kernels directly and never reach the merge.
 #pragma once
 
 #include <cuda_bf16.h>

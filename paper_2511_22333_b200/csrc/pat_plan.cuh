@@ -51,13 +51,16 @@ struct DevPlan {
   const int32_t* unit_slot;     // slot id per (unit, member) or -1 = write output directly
   const Item* items[NUM_VARIANTS];
   const int32_t* n_items;       // [NUM_VARIANTS] (device counts)
+  const int32_t* n_pair;        // [NUM_VARIANTS] leading items of > 128 rows (tcgen05: run by both
+                                //     item pipelines of a CTA on one KV stream)
   const int32_t* merge_q;       // [n_merge_q] queries with > 1 unit
   const int4* merge_desc;       // [n_merge_q] (query, first slot, slots, 0): one load per merge row
   const int32_t* q_slot_off;    // [B] first slot of the query
   const int32_t* q_nslot;       // [B] slots of the query (0 or >= 2)
   const int32_t* n_merge;       // [1]
-  int32_t* sched;               // [2] dynamic item counter, finished CTAs (tcgen05 kernel;
-                                //     zero between launches: the last CTA resets them)
+  int32_t* sched;               // [4] dynamic item counters (pair items, finished CTAs, other
+                                //     items; tcgen05 kernel; zero between launches: the last CTA
+                                //     resets them)
   int32_t H, KVH, d, G, bs;
 };
 

@@ -26,6 +26,7 @@ struct HostSchedule {
   std::vector<int32_t> unit_slot_off, unit_slot;
   std::vector<int32_t> q_slot_off, q_nslot, merge_q;
   std::vector<Item> items[NUM_VARIANTS];
+  int32_t n_pair[NUM_VARIANTS] = {0, 0, 0, 0};  // leading pair items (> 128 rows, tcgen05)
   double work[NUM_VARIANTS] = {0, 0, 0, 0};  // estimated SM-ns per kernel variant
   int32_t n_slots = 0;
 };
@@ -37,9 +38,11 @@ int64_t distinct_tokens(const RowsView& R);
 struct ScheduleParams {
   int B, bs, H, KVH, d, split_mode, num_sms;
   int tc_min_rows;  // rows threshold of the tcgen05 variant (0 = off)
+  bool pair_items = false;  // PAT_PLAN_PAIR_ITEMS
+  pat_cost_model cm{};      // snapshot of the cost model (host_schedule takes it)
 };
 int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* out);
 // process-wide scheduler cost model (pat_set_cost_model)
-const pat_cost_model& cost_model();
+pat_cost_model cost_model();  // a copy taken under the model's lock
 
 }  // namespace pat

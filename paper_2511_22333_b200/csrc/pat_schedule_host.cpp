@@ -23,7 +23,10 @@ static pat_cost_model g_cost_model = {1200.0, 2000.0, 1440.0, 1500.0, 6.5e3};
 constexpr int kTcLanesPerSm = 2;  // independent item pipelines per tcgen05 CTA
 static std::mutex g_cost_mu;
 
-const pat_cost_model& cost_model() { return g_cost_model; }
+pat_cost_model cost_model() {
+  std::lock_guard<std::mutex> lk(g_cost_mu);
+  return g_cost_model;
+}
 
 namespace {
 
@@ -51,7 +54,7 @@ void split_pack(int npages, int kv, int bs, int parts, std::vector<Part>& out) {
 // chip's ~7 TB/s L2 -> SM bandwidth) plus the item boundary (Q load, last PV,
 // epilogue stores); the mma.sync streaming kernel is HBM-paced.
 double item_ns(const ScheduleParams& sp, int v, int rows, int ntok) {
-  const pat_cost_model& cm = cost_model();
+  const pat_cost_model& cm = sp.cm;
   const double steps = (double)ceil_div(ntok, 64);
   const double dscale = sp.d / 128.0;
   if (v == VAR_TC)
@@ -84,7 +87,7 @@ double lpt_makespan(std::vector<double>& costs, int lanes) {
 void native_parts(const HostPacks& P, const ScheduleParams& sp, std::vector<int>& nparts) {
   const int NP = P.n_packs();
   const int G = sp.H / sp.KVH;
-  const double bw = cost_model().hbm_bytes_per_ns;
+  const double bw = sp.cm.hbm_bytes_per_ns;
   std::vector<int> rows(NP), pages(NP);
   int maxpages = 1;
   double kv_bytes = 0;
@@ -161,7 +164,9 @@ void native_parts(const HostPacks& P, const ScheduleParams& sp, std::vector<int>
 
 }  // namespace
 
-int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S) {
+int host_schedule(const HostPacks& P, const ScheduleParams& sp_in, HostSchedule* S) {
+  ScheduleParams sp = sp_in;
+  sp.cm = cost_model();  // one consistent snapshot for the whole schedule
   const int NP = P.n_packs();
   const int G = sp.H / sp.KVH;
   *S = HostSchedule();
@@ -244,19 +249,28 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* S)
     int p = S->unit_pack[u];
     int rows = (P.q_off[p + 1] - P.q_off[p]) * G;
     int v = choose_variant(rows, sp.tc_min_rows);
-    int R = variant_rows(v);
+    // tcgen05: rows of a wide pack go in 256-row pair items (both item
+    // pipelines of a CTA share one KV stream: half the L2 -> SM bytes per row)
+    int R = sp.pair_items && v == VAR_TC && rows > variant_rows(v) ? 2 * variant_rows(v) : variant_rows(v);
     for (int r0 = 0; r0 < rows; r0 += R) {
-      const double ns = item_ns(sp, v, std::min(R, rows - r0), S->unit_ntok[u]);
+      const int n = std::min(R, rows - r0);
+      const double ns = item_ns(sp, v, std::min(n, variant_rows(v)), S->unit_ntok[u]);
       for (int h = 0; h < sp.KVH; ++h)
-        cands.push_back({{u, h, r0, std::min(R, rows - r0), P.blk_off[p] + S->unit_page0[u], S->unit_ntok[u],
-                          P.q_off[p], S->unit_slot_off[u]},
+        cands.push_back({{u, h, r0, n, P.blk_off[p] + S->unit_page0[u], S->unit_ntok[u], P.q_off[p],
+                          S->unit_slot_off[u]},
                          ns, v});
     }
   }
-  std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.ns > b.ns; });
+  // pair items first (the kernel runs them in a first phase), then longest first
+  auto is_pair = [](const Cand& c) { return c.v == VAR_TC && c.it.nrows > variant_rows(VAR_TC); };
+  std::stable_sort(cands.begin(), cands.end(), [&](const Cand& a, const Cand& b) {
+    if (is_pair(a) != is_pair(b)) return is_pair(a);
+    return a.ns > b.ns;
+  });
   for (const Cand& c : cands) {
     S->items[c.v].push_back(c.it);
-    S->work[c.v] += c.ns;
+    S->work[c.v] += c.ns * (is_pair(c) ? 2 : 1);
+    if (is_pair(c)) S->n_pair[c.v]++;
   }
   (void)unit_begin;
   return PAT_OK;

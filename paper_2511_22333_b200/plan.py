@@ -33,22 +33,28 @@ class PatPlan:
         self.num_heads = num_heads
         self.num_kv_heads = num_kv_heads
         self.head_dim = head_dim
+        inf = self.info()
+        self.num_queries = int(inf.num_queries)  # rows of q / out the kernels index
+        self.block_size = int(inf.block_size)    # page size the KV tensor maps use
 
     # -- construction ---------------------------------------------------------------
     @staticmethod
-    def _opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms=0, tc_min_rows=0, forward_only=False):
+    def _opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms=0, tc_min_rows=0, forward_only=False,
+              pair_items=False):
         if split not in N.SPLIT_MODES:
             raise InvalidSpec(f"split must be one of {sorted(N.SPLIT_MODES)}")
-        flags = (N.PAT_PLAN_HOST_ONLY if host_only else 0) | (N.PAT_PLAN_FORWARD_ONLY if forward_only else 0)
+        flags = (N.PAT_PLAN_HOST_ONLY if host_only else 0) | (N.PAT_PLAN_FORWARD_ONLY if forward_only else 0) | \
+            (N.PAT_PLAN_PAIR_ITEMS if pair_items else 0)
         return N.PlanOptions(num_heads, num_kv_heads, head_dim, N.SPLIT_MODES[split], num_sms, flags, tc_min_rows)
 
     @classmethod
     def from_table(cls, table, num_heads=32, num_kv_heads=8, head_dim=128, split="native", host_only=False,
-                   num_sms=0, tc_min_rows=0, forward_only=False) -> "PatPlan":
+                   num_sms=0, tc_min_rows=0, forward_only=False, pair_items=False) -> "PatPlan":
         """Host C++ packer (``pat_plan_create_host``) on a BlockTable.  ``forward_only``:
-        timing aid, ``pat_forward`` skips the merge."""
+        timing aid, ``pat_forward`` skips the merge.  ``pair_items``: PAT_PLAN_PAIR_ITEMS."""
         off, blk, valid = table.csr()
-        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms, tc_min_rows, forward_only)
+        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms, tc_min_rows, forward_only,
+                        pair_items)
         h = C.c_void_p()
         st = N.lib().pat_plan_create_host(len(table.rows), N.ptr(off, C.c_int64), N.ptr(blk, C.c_int32),
                                           N.ptr(valid, C.c_int32), table.block_size, C.byref(opt), C.byref(h))

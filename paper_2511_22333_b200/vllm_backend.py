@@ -20,7 +20,8 @@ from __future__ import annotations
 
 import torch
 
-from vllm.v1.attention.backends.flash_attn import FlashAttentionBackend, FlashAttentionImpl
+from vllm.v1.attention.backends.flash_attn import (FlashAttentionBackend, FlashAttentionImpl,
+                                                   FlashAttentionMetadataBuilder)
 
 from .torch_op import decode_attention  # noqa: F401  (registers the op)
 
@@ -28,6 +29,21 @@ try:  # vLLM >= 0.11 location of AttentionType
     from vllm.attention.backends.abstract import AttentionType
 except Exception:  # pragma: no cover
     from vllm.v1.attention.backend import AttentionType  # type: ignore
+from vllm.v1.attention.backend import AttentionCGSupport
+
+
+class PatAttentionMetadataBuilder(FlashAttentionMetadataBuilder):
+    """FlashAttention's metadata with full-CUDA-graph capture of attention turned
+    off: the PAT op looks its plan up by a device fingerprint of the block table
+    that the host reads back, and packs a new plan on a miss -- host work a
+    captured graph would freeze (vLLM then runs attention eagerly between its
+    piecewise graphs)."""
+
+    _cudagraph_support = AttentionCGSupport.NEVER
+
+    @classmethod
+    def get_cudagraph_support(cls, vllm_config, kv_cache_spec) -> AttentionCGSupport:
+        return AttentionCGSupport.NEVER
 
 
 class PatAttentionImpl(FlashAttentionImpl):
@@ -45,7 +61,8 @@ class PatAttentionImpl(FlashAttentionImpl):
                 output_block_scale=None):
         if output_scale is None and output_block_scale is None and self._pat_eligible(kv_cache, attn_metadata):
             n = attn_metadata.num_actual_tokens
-            q = query[:n].view(n, self.num_heads, self.head_size)
+            # the query is usually a strided view of the fused qkv projection
+            q = query[:n].reshape(n, self.num_heads, self.head_size).contiguous()
             out = output[:n].view(n, self.num_heads, self.head_size)
             torch.ops.patb200.decode_attention(q, kv_cache[0], kv_cache[1], attn_metadata.block_table[:n],
                                                attn_metadata.seq_lens[:n], out, self.scale)
@@ -63,6 +80,10 @@ class PatAttentionBackend(FlashAttentionBackend):
     def get_impl_cls() -> type[PatAttentionImpl]:
         return PatAttentionImpl
 
+    @staticmethod
+    def get_builder_cls() -> type[PatAttentionMetadataBuilder]:
+        return PatAttentionMetadataBuilder
+
 
 def register() -> None:
     """Register PatAttentionBackend as vLLM's CUSTOM attention backend."""
@@ -71,4 +92,4 @@ def register() -> None:
     register_backend(AttentionBackendEnum.CUSTOM, f"{__name__}.PatAttentionBackend")
 
 
-__all__ = ["PatAttentionBackend", "PatAttentionImpl", "register"]
+__all__ = ["PatAttentionBackend", "PatAttentionImpl", "PatAttentionMetadataBuilder", "register"]

@@ -12,6 +12,8 @@ from paper_2511_22333_b200.plan import PatPlan
 
 from golden_io import as_packs, config_cases, family_cases, random_cases
 
+from gpu_ref import check_close, full_attention_gpu  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 
@@ -115,7 +117,8 @@ def test_device_lazy_update():
 
 
 def test_torch_op_decode_attention():
-    """torch.ops.patb200.decode_attention (vLLM-style tensors) == pat_attention."""
+    """torch.ops.patb200.decode_attention (vLLM-style tensors) against the float64
+    reference (full_attention, attention.py:70-102), and == pat_attention."""
     w = configs.workload("c1")
     table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
     bt_np, sl_np = table.padded()
@@ -129,11 +132,14 @@ def test_torch_op_decode_attention():
     plan = PatPlan.from_table(table, 32, 8, 128)
     ref = P.pat_attention(plan, q, kv[0].contiguous(), kv[1].contiguous())
     torch.cuda.synchronize()
+    check_close(out, full_attention_gpu(q, kv[0], kv[1], w.rows, w.valid_last, w.block_size), "torch op")
     assert torch.equal(out, ref)
 
 
 def test_vllm_backend_decode_matches_pat():
-    """PatAttentionImpl (vLLM CUSTOM backend) on a decode-only batch == pat_attention."""
+    """PatAttentionImpl (vLLM CUSTOM backend) on a decode-only batch whose query is a
+    strided slice of a fused qkv buffer, against the float64 reference and
+    == pat_attention; its metadata builder opts out of full CUDA-graph capture."""
     vllm_backend = pytest.importorskip("paper_2511_22333_b200.vllm_backend")
     from types import SimpleNamespace
 
@@ -147,13 +153,22 @@ def test_vllm_backend_decode_matches_pat():
     impl = vllm_backend.PatAttentionImpl(32, 128, 128 ** -0.5, 8, None, None, "auto")
     meta = SimpleNamespace(max_query_len=1, use_cascade=False, num_actual_tokens=w.batch,
                            block_table=torch.from_numpy(bt_np).cuda(), seq_lens=torch.from_numpy(sl_np).cuda())
+    qkv = torch.zeros(w.batch, (32 + 2 * 8) * 128, device="cuda", dtype=torch.bfloat16)
+    qkv[:, :32 * 128] = q.view(w.batch, -1)
+    query = qkv[:, :32 * 128]  # strided view, as vLLM splits the fused projection
+    assert not query.is_contiguous()
     output = torch.empty(w.batch, 32 * 128, device="cuda", dtype=torch.bfloat16)
-    impl.forward(None, q.view(w.batch, -1), None, None, kv, meta, output)
-    impl.forward(None, q.view(w.batch, -1), None, None, kv, meta, output)  # plan reused (identity fast path)
+    impl.forward(None, query, None, None, kv, meta, output)
+    impl.forward(None, query, None, None, kv, meta, output)  # plan reused (identity fast path)
     plan = PatPlan.from_table(table, 32, 8, 128)
     ref = P.pat_attention(plan, q, kv[0], kv[1])
     torch.cuda.synchronize()
+    check_close(output.view(w.batch, 32, 128), full_attention_gpu(q, kv[0], kv[1], w.rows, w.valid_last,
+                                                                   w.block_size), "vllm backend")
     assert torch.equal(output.view(w.batch, 32, 128), ref)
+    from vllm.v1.attention.backend import AttentionCGSupport
+    builder = vllm_backend.PatAttentionBackend.get_builder_cls()
+    assert builder.get_cudagraph_support(None, None) == AttentionCGSupport.NEVER
 
 
 def test_cli_run_and_verify(tmp_path, capsys):

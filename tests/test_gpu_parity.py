@@ -152,3 +152,28 @@ def test_errors_map_to_reference_exceptions():
         P.run_packed_attention(t, P.pack_batch(t).packs[:-1], store, q, spec64)
     with pytest.raises(P.ShapeMismatch):
         P.run_packed_attention(t, P.pack_batch(t), store, q[:1], spec64)
+
+
+def test_shape_checks_raise_shape_mismatch():
+    """q rows, out shape/dtype and the cache page size are checked
+    against the plan before any launch (reference: ShapeMismatch, attention.py:220)."""
+    from paper_2511_22333_b200.errors import ShapeMismatch
+    w = configs.workload("c1")
+    table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    plan = PatPlan.from_table(table, 32, 8, 128)
+    nb = w.num_pool_blocks()
+    kc = torch.zeros(nb, 16, 8, 128, device="cuda", dtype=torch.float16)
+    q = torch.zeros(w.batch, 32, 128, device="cuda", dtype=torch.float16)
+    with pytest.raises(ShapeMismatch):
+        P.pat_attention(plan, q[:-1].contiguous(), kc, kc)
+    with pytest.raises(ShapeMismatch):
+        P.pat_attention(plan, q, kc, kc, out=torch.empty(w.batch, 32, 128, device="cuda", dtype=torch.bfloat16))
+    with pytest.raises(ShapeMismatch):
+        k8 = torch.zeros(2 * nb, 8, 8, 128, device="cuda", dtype=torch.float16)
+        P.pat_attention(plan, q, k8, k8)
+    dec = P.PatDecoder(32, 8, 128)
+    bt_np, sl_np = table.padded()
+    with pytest.raises(ShapeMismatch):
+        dec.forward_device(torch.from_numpy(bt_np).cuda(), torch.from_numpy(sl_np).cuda(), q[:-1].contiguous(),
+                           kc, kc)
+    plan.close()

@@ -37,7 +37,8 @@ def run(name, tc_min_rows=0):
                                 forward_only=True)
     out = torch.empty_like(q)
     ws = torch.zeros(max(plan.workspace_bytes(), 256), dtype=torch.uint8, device="cuda")
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    import bench
+    flush = bench.L2Flush("cuda")
     lib = N.lib()
     lib.pat_debug_item_log.argtypes = [C.c_void_p, C.c_void_p]
     log = np.zeros((32768, 8), dtype=np.int64)

@@ -77,7 +77,8 @@ def main():
     ap.add_argument("--mode", default="hbm,l2")
     ap.add_argument("--tc", type=int, default=1, help="tc_min_rows (1: every pack on the tcgen05 kernel)")
     args = ap.parse_args()
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    import bench
+    flush = bench.L2Flush("cuda")
     for rows in [int(x) for x in args.rows.split(",")]:
         line = f"rows {rows:4d}"
         for mode in args.mode.split(","):
