@@ -27,7 +27,18 @@
 // columns of packed 16-bit pairs written over the consumed S), Q at +64
 // (packed pairs, the A operand of QK), O at +128.
 // KV tiles are 32 tokens (16 KB stages, 6 per lane): a stage is released as
-// soon as its PV completes, so more of the ring is in flight.
+// soon as its PV completes, so more of the ring is in flight.  The ring is laid
+// out as K and V planes ([64 d][6 stages x 32 tokens] x 128 B each), so two
+// consecutive stages hold 64 contiguous token rows.
+//
+// Narrow items (<= 16 rows: the unshared suffixes of a batch) would leave 112
+// of the 128 MMA rows idle.  They run transposed instead, on 64-token tiles
+// (an even/odd stage pair; the producer aligns them):
+//   S^T[b] = K Q^T     (SS: M = 128 token rows -- 64 live --, N = 16 rows, K = d)
+//   O^T   += V^T P^T   (SS: M = d, N = 16 rows, K = tokens; P^T in smem)
+// a thread per token for the softmax (per-row maxima shared through a
+// barrier-reduction vote and, when a row's max grows, shared memory) and a
+// thread per head-dim lane for the epilogue: ~6x fewer tensor cycles per token.
 // Numerics follow cta_partial (attention.py:140-163): fp32 scores and
 // accumulators, log2-domain online softmax with lazy O rescale (only when the
 // running max grows by > 8), bf16 P = hi + lo (two PV MMAs), fp16 P single and
@@ -51,7 +62,7 @@ __device__ int g_trace_cta;
 __device__ unsigned long long g_span_tc[1][kSpanCtas][2];
 // per-item log (all CTAs, both lanes): cta*2+lane, item, rows, tiles, t_start, t_first_data, t_tiles_done, t_epi_done
 constexpr int kItemLog = 32768;
-__device__ long long g_item_log[kItemLog][8];
+__device__ long long g_item_log[kItemLog][12];  // + [8] Q stored, [9] last PV done, [10] O read
 __device__ int g_item_n;
 __device__ __forceinline__ long long gtime() {
   long long t;
@@ -84,6 +95,9 @@ constexpr int kN = 32;   // tokens per KV tile
 constexpr int kStages = PAT_TC4_STAGES;  // per lane
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kNarrow = 16;                // items of <= 16 rows run transposed (N = 16)
+constexpr int kNN = 2 * kN;                // tokens per narrow tile (a stage pair)
+static_assert(kStages % 2 == 0, "narrow tiles are aligned stage pairs");
 
 struct ItemSlot {
   int32_t idx;
@@ -98,14 +112,20 @@ constexpr uint32_t kFIdx = 0, kFShared = 4, kFG0 = 8, kFKvh = 32 + 4, kFRow0 = 3
 template <int D>
 struct Layout {
   static constexpr int KB = D / 64;
-  static constexpr int kTileBytes = KB * kN * 128;  // K or V stage tile: [KB][32 tok][128 B]
-  static constexpr int kLaneRing = kStages * 2 * kTileBytes;
-  static constexpr int kOffKV = 0;  // lane L ring at L * kLaneRing
+  static constexpr int kPlane = kStages * kN * 128;  // one 64-d plane of K or V: [6 x 32 tokens][128 B]
+  static constexpr int kLaneRing = 2 * KB * kPlane;  // K planes, then V planes
+  static constexpr int kOffKV = 0;                   // lane L ring at L * kLaneRing
   static constexpr int kOffBar = 2 * kLaneRing;
   static constexpr int kOffRing = kOffBar + 1024;  // item slots [lane][2]
-  static constexpr int kBytes = kOffRing + 4 * (int)sizeof(ItemSlot);
+  // narrow items, per lane: Q rows [KB][16][128 B], P^T [2 buffers][hi, lo][16 rows][64 tokens x 2 B]
+  static constexpr int kNarQ = KB * kNarrow * 128;
+  static constexpr int kNarLane = kNarQ + 4 * kNarrow * 128;
+  static constexpr int kOffNar = (kOffRing + 4 * (int)sizeof(ItemSlot) + 1023) / 1024 * 1024;
+  static constexpr int kOffX = kOffNar + 2 * kNarLane;  // [lane][max, sum][2 warps][16] floats
+  static constexpr int kBytes = kOffX + 2 * 2 * 2 * kNarrow * 4;
   static constexpr int kAlloc = kBytes + 1024;
   static_assert(kAlloc <= 227 * 1024, "shared memory budget");
+  static_assert(kNarQ % 1024 == 0, "SW128 operands are 1024-byte aligned");
 };
 
 enum Bar : int {
@@ -136,6 +156,7 @@ template <> struct Fmt<__half> {
   static __device__ __forceinline__ float2 unpack(uint32_t v) {
     return __half22float2(*reinterpret_cast<__half2*>(&v));
   }
+  static __device__ __forceinline__ __half cvt(float a) { return __float2half_rn(a); }
 };
 template <> struct Fmt<__nv_bfloat16> {
   static constexpr int ab = 1;
@@ -151,11 +172,18 @@ template <> struct Fmt<__nv_bfloat16> {
   static __device__ __forceinline__ float2 unpack(uint32_t v) {
     return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
   }
+  static __device__ __forceinline__ __nv_bfloat16 cvt(float a) { return __float2bfloat16_rn(a); }
 };
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
+}
+__device__ __forceinline__ float4 lds_v4f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+               : "memory");
+  return v;
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
@@ -180,6 +208,34 @@ __device__ __forceinline__ int2 lds_v2(uint32_t a) {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void sts_u16(uint32_t a, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+// named barrier of n threads that ORs a predicate across them
+__device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t n, bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.u32 q, %3, 0;\n bar.red.or.pred p, %1, %2, q;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(r)
+      : "r"(id), "r"(n), "r"((uint32_t)v)
+      : "memory");
+  return r != 0;
+}
+// Instruction descriptor, kind::f16, fp32 accumulate, with both operand majors.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int ab_fmt, int a_mn_major, int b_mn_major) {
+  return (1u << 4) | ((uint32_t)ab_fmt << 7) | ((uint32_t)ab_fmt << 10) | ((uint32_t)a_mn_major << 15) |
+         ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ uint16_t bits16(uint32_t packed_lo) { return (uint16_t)(packed_lo & 0xffffu); }
+
 __device__ __forceinline__ Item load_item(const Item* p) {
   const int4* q = reinterpret_cast<const int4*>(p);
   int4 a = __ldg(q), b = __ldg(q + 1);
@@ -210,9 +266,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int pl = warp < 4 ? (warp >> 1) : ((warp - 4) >> 2);
   auto barL = [&](int l, int i) { return sb + L::kOffBar + (uint32_t)((l * BARS_PER_LANE + i) * 8); };
   auto bar = [&](int i) { return barL(pl, i); };
-  // stage s of lane l's KV ring
-  auto sK = [&](int l, int s) { return sb + L::kOffKV + (uint32_t)(l * L::kLaneRing + s * 2 * L::kTileBytes); };
-  auto sV = [&](int l, int s) { return sK(l, s) + (uint32_t)L::kTileBytes; };
+  // stage s of lane l's KV ring: K at sK(l, s) + kb * kPlane, V likewise
+  auto sK = [&](int l, int s) { return sb + L::kOffKV + (uint32_t)(l * L::kLaneRing + s * kN * 128); };
+  auto sV = [&](int l, int s) { return sK(l, s) + (uint32_t)(KB * L::kPlane); };
+  // narrow items: Q rows (B of S^T = K Q^T), P^T (B of O^T = V^T P^T), row max / sum exchange
+  const uint32_t sQn = sb + L::kOffNar + (uint32_t)(pl * L::kNarLane);
+  auto sPn = [&](uint32_t b, int h) { return sQn + (uint32_t)(L::kNarQ + (int)(b * 2 + h) * kNarrow * 128); };
+  const uint32_t xch = sb + L::kOffX + (uint32_t)(pl * 2 * 2 * kNarrow * 4);
   int2* join = reinterpret_cast<int2*>(smem + L::kOffBar + 2 * BARS_PER_LANE * 8 + 16);  // [2] mailbox
   const uint32_t ring_s = sb + L::kOffRing + (uint32_t)(pl * 2 * kSlotBytes);
   ItemSlot* ring = reinterpret_cast<ItemSlot*>(smem + L::kOffRing) + pl * 2;
@@ -324,6 +384,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_prefetch_l2(qg + ((int64_t)qid * H + item.kvh * G + (a - i * G)) * D, (uint32_t)((e - a) * D * 2));
           }
         }
+        // first ring position of the item: narrow items start on an even stage
+        // (their 64-token tiles are stage pairs); the odd one is skipped
+        const bool narrow = it >= 0 && !shared && item.nrows <= kNarrow;
+        if (!shared) g0 = narrow ? ((gt + 1) & ~1u) : gt;
         if (lane == 0) {
           ring[slot].idx = it;
           ring[slot].pad[0] = shared;
@@ -333,6 +397,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(bar(ITEM_FULL + slot));
         if (it < 0) break;
         if (shared) continue;  // the tiles come through lane 0's ring
+        if (g0 != gt) {  // skipped stage: an empty phase (no bytes), released by the MMA warp
+          const int s = gt % kStages;
+          mbar_wait(bar(KV_EMPTY + s), ((gt / kStages) & 1) ^ 1);
+          if (gt >= (uint32_t)kStages && gt - kStages < pair_upto)
+            mbar_wait(bar(XKV_EMPTY + s), ((gt / kStages) & 1) ^ 1);
+          if (elect_one()) mbar_arrive(bar(KV_FULL + s));
+          __syncwarp();
+          ++gt;
+        }
         const int h = item.kvh, ntok = item.ntok;
         const int32_t* blist = plan.pack_blk + item.blk;
         const int ntiles = (ntok + kN - 1) / kN;
@@ -363,8 +436,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (elect_one()) {
 #pragma unroll
               for (int kb = 0; kb < KB; ++kb) {
-                tma_load_4d(sK(pl, s) + kb * (kN * 128) + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
-                tma_load_4d(sV(pl, s) + kb * (kN * 128) + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
+                tma_load_4d(sK(pl, s) + kb * L::kPlane + gr * 2048, &tmk, bar(KV_FULL + s), kb * 64, h, off, blk);
+                tma_load_4d(sV(pl, s) + kb * L::kPlane + gr * 2048, &tmv, bar(KV_FULL + s), kb * 64, h, off, blk);
               }
             }
             __syncwarp();
@@ -373,42 +446,65 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else {
       // ------------------------------------------------------------ MMA issuer
-      // Per lane tile c (S/P buffer b = c & 1): QK(c) needs its KV stage and
+      // Per lane tile c (S/P buffer b = c & 1): QK(c) needs its KV stage(s) and
       // PV(c-2) done (it read P[b], which QK(c) overwrites); QK runs one tile
       // ahead of PV, so the softmax of tile c overlaps QK(c+1).  The stage of
-      // tile t of an item is ring position base + t of the lane's own ring, or
-      // of lane 0's ring for a joined pair item.
+      // ring position g is g % kStages of the lane's own ring, or of lane 0's
+      // ring for a joined pair item.  (Issuing PV from the softmax warpgroup
+      // after a named barrier instead measured slower: c4 219 -> 246 us.)
       constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
       constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
+      constexpr uint32_t idesc_qkn = idesc_f16(kM, kNarrow, Fmt<T>::ab, 0, 0);  // S^T = K Q^T
+      constexpr uint32_t idesc_pvn = idesc_f16(kM, kNarrow, Fmt<T>::ab, 1, 0);  // O^T = V^T P^T
       uint32_t tcnt = 0, rpos = 0, qu = 0, ou = 0;
       for (uint32_t n = 0;; ++n) {
         mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1);
         const int it = fld(n, kFIdx);
         const int ntok = it >= 0 ? fld(n, kFNtok) : 0;
+        const bool narrow = it >= 0 && !fld(n, kFShared) && fld(n, kFNrows) <= kNarrow;
         const int src = it >= 0 && fld(n, kFShared) ? 0 : pl;  // ring the tiles come from
-        const uint32_t base = src != pl ? (uint32_t)fld(n, kFG0) : rpos;
+        const uint32_t base = it >= 0 ? (uint32_t)fld(n, kFG0) : 0u;
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
         if (it < 0) break;
-        const int ntiles = (ntok + kN - 1) / kN;
+        if (src == pl && base != rpos) {  // a stage the producer skipped to align a narrow item
+          const int s = (int)(rpos % kStages);
+          mbar_wait(bar(KV_FULL + s), (rpos / kStages) & 1);
+          if (elect_one()) mbar_arrive(bar(KV_EMPTY + s));
+          __syncwarp();
+          rpos = base;
+        }
+        const int ntiles = narrow ? (ntok + kNN - 1) / kNN : (ntok + kN - 1) / kN;
         auto qk = [&](int t, bool first) {
-          const uint32_t g = base + (uint32_t)t, c = tcnt + (uint32_t)t, b = c & 1;
+          const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
+          const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
           const int s = (int)(g % kStages);
           if (pl == 0) TC_TRACE(1, 2, c);
           mbar_wait(barL(src, KV_FULL + s), (g / kStages) & 1);
+          if (narrow && ntok - t * kNN > kN) mbar_wait(barL(src, KV_FULL + s + 1), ((g + 1) / kStages) & 1);
           if (pl == 0) TC_TRACE(1, 3, c);
           mbar_wait(bar(SP_FREE + b), ((c >> 1) & 1) ^ 1);
           if (first) mbar_wait(bar(QT_FULL), qu++ & 1);
           tc_fence_after();
           if (pl == 0) TC_TRACE(1, 0, c);
           if (elect_one()) {
-            const uint64_t k0 = umma_desc_sw128(sK(src, s), 16, 1024);
+            if (narrow) {
 #pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const int kb = k >> 2, kk = k & 3;
-              // Q(m, k) packed two per column: a k-step of 16 = 8 columns
-              umma_f16_ts(tg + 32u * b, tg + 64u + (uint32_t)(k * 8),
-                          k0 + (uint64_t)((kb * (kN * 128) + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
+              for (int k = 0; k < D / 16; ++k) {
+                const int kb = k >> 2, kk = k & 3;
+                const uint64_t ad = umma_desc_sw128(sK(src, s) + (uint32_t)(kb * L::kPlane + kk * 32), 16, 1024);
+                const uint64_t bd = umma_desc_sw128(sQn + (uint32_t)(kb * kNarrow * 128 + kk * 32), 16, 1024);
+                umma_f16_ss(tg + 32u * b, ad, bd, idesc_qkn, k > 0 ? 1u : 0u);
+              }
+            } else {
+              const uint64_t k0 = umma_desc_sw128(sK(src, s), 16, 1024);
+#pragma unroll
+              for (int k = 0; k < D / 16; ++k) {
+                const int kb = k >> 2, kk = k & 3;
+                // Q(m, k) packed two per column: a k-step of 16 = 8 columns
+                umma_f16_ts(tg + 32u * b, tg + 64u + (uint32_t)(k * 8),
+                            k0 + (uint64_t)((kb * L::kPlane + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
+              }
             }
             umma_commit(bar(S_FULL + b));
           }
@@ -416,63 +512,108 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         qk(0, true);
         for (int t = 0; t < ntiles; ++t) {
-          const uint32_t g = base + (uint32_t)t, c = tcnt + (uint32_t)t, b = c & 1;
+          const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
+          const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
+          const int s = (int)(g % kStages);
           if (t + 1 < ntiles) qk(t + 1, false);
           if (pl == 0) TC_TRACE(1, 4, c);
           mbar_wait(bar(P_FULL + b), (c >> 1) & 1);
           if (t == 0) mbar_wait(bar(O_EMPTY), (ou & 1) ^ 1);
           tc_fence_after();
           if (elect_one()) {
-            const int s = (int)(g % kStages);
-            const uint64_t v0 = umma_desc_sw128(sV(src, s), kN * 128, 1024);
+            const uint32_t rel = src != pl ? barL(0, XKV_EMPTY + s) : bar(KV_EMPTY + s);
+            if (narrow) {
+              const int vt = min(kNN, ntok - t * kNN);
+              const int nk = (vt + 15) / 16;
+              for (int j = 0; j < nk; ++j) {
+                const uint64_t ad = umma_desc_sw128(sV(src, s) + (uint32_t)(j * 16 * 128), L::kPlane, 1024);
+                umma_f16_ss(tg + 128u, ad, umma_desc_sw128(sPn(b, 0) + (uint32_t)(j * 32), 16, 1024), idesc_pvn,
+                            (t == 0 && j == 0) ? 0u : 1u);
+                if constexpr (kSplit)
+                  umma_f16_ss(tg + 128u, ad, umma_desc_sw128(sPn(b, 1) + (uint32_t)(j * 32), 16, 1024), idesc_pvn,
+                              1u);
+              }
+              umma_commit(bar(SP_FREE + b));
+              umma_commit(rel);
+              if (vt > kN) umma_commit(bar(KV_EMPTY + s + 1));
+            } else {
+              const uint64_t v0 = umma_desc_sw128(sV(src, s), L::kPlane, 1024);
 #pragma unroll
-            for (int k = 0; k < kN / 16; ++k) {
-              const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
-              // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
-              umma_f16_ts(tg + 128u, tg + 32u * b + (uint32_t)(k * 8), bd, idesc_pv, (t == 0 && k == 0) ? 0u : 1u);
-              if constexpr (kSplit)
-                umma_f16_ts(tg + 128u, tg + 32u * b + 16u + (uint32_t)(k * 8), bd, idesc_pv, 1u);
+              for (int k = 0; k < kN / 16; ++k) {
+                const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
+                // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
+                umma_f16_ts(tg + 128u, tg + 32u * b + (uint32_t)(k * 8), bd, idesc_pv, (t == 0 && k == 0) ? 0u : 1u);
+                if constexpr (kSplit)
+                  umma_f16_ts(tg + 128u, tg + 32u * b + 16u + (uint32_t)(k * 8), bd, idesc_pv, 1u);
+              }
+              umma_commit(bar(SP_FREE + b));
+              umma_commit(rel);
             }
-            umma_commit(bar(SP_FREE + b));
-            umma_commit(src != pl ? barL(0, XKV_EMPTY + s) : bar(KV_EMPTY + s));
           }
           __syncwarp();
           if (pl == 0) TC_TRACE(1, 1, c);
         }
         ++ou;
         tcnt += (uint32_t)ntiles;
-        if (src == pl) rpos += (uint32_t)ntiles;
+        if (src == pl) rpos = base + (uint32_t)((ntok + kN - 1) / kN);
       }
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
     const int wq = warp & 3;          // TMEM lane quarter
-    const int ln = wq * 32 + lane;    // TMEM lane = row of the item
+    const int ln = wq * 32 + lane;    // TMEM lane: row of a regular item, token of a narrow tile
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t sp = tg + lane_base;
+    const uint32_t nbar = 1 + (uint32_t)pl;  // named barrier of the lane's 128 softmax threads
+    constexpr int CPT = D / 64;              // 16-byte chunks of a narrow item's Q tile per thread
 #ifdef PAT_TC_TRACE
     const bool tr = (wq == 0 && lane == 0);
 #endif
-    uint32_t tcnt = 0, rpos = 0;  // tiles consumed (S/P phases), own ring position
+    uint32_t tcnt = 0;  // tiles consumed by this lane (S/P phases)
 
     auto wait_item = [&](uint32_t n) { mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1); };
-    // this thread's Q row of item n (zeros past the item's rows) into registers
+    auto q_row = [&](uint32_t n, int r) {
+      const int qid = fld(n, kFMeta + 8 * r);
+      const int head = fld(n, kFKvh) * G + (fld(n, kFRow0) + r) % G;
+      return reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + head) * D);
+    };
+    // Q of item n into registers (zeros past its rows): a regular item's row
+    // `ln` (D / 2 words), or CPT 16-byte chunks of a narrow item's 16-row tile
+    // narrow (transposed) items: <= 16 rows, tiles from the lane's own ring
+    auto is_narrow = [&](uint32_t n) { return fld(n, kFNrows) <= kNarrow && !fld(n, kFShared); };
     auto load_q = [&](uint32_t n, uint32_t* qv) {
-      const bool live = ln < fld(n, kFNrows);
-      const uint4* src = nullptr;
-      if (live) {
-        const int qid = fld(n, kFMeta + 8 * ln);
-        const int head = fld(n, kFKvh) * G + (fld(n, kFRow0) + ln) % G;
-        src = reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + head) * D);
-      }
+      const int nr = fld(n, kFNrows);
+      if (is_narrow(n)) {
+        const int r = ln >> 3;
+        const uint4* src = r < nr ? q_row(n, r) : nullptr;
 #pragma unroll
-      for (int i = 0; i < D / 8; ++i) {
-        const uint4 v = live ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
-        qv[4 * i] = v.x, qv[4 * i + 1] = v.y, qv[4 * i + 2] = v.z, qv[4 * i + 3] = v.w;
+        for (int i = 0; i < CPT; ++i) {
+          const uint4 v = src ? __ldg(src + (ln & 7) * CPT + i) : make_uint4(0, 0, 0, 0);
+          qv[4 * i] = v.x, qv[4 * i + 1] = v.y, qv[4 * i + 2] = v.z, qv[4 * i + 3] = v.w;
+        }
+      } else {
+        const uint4* src = ln < nr ? q_row(n, ln) : nullptr;
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i) {
+          const uint4 v = src ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+          qv[4 * i] = v.x, qv[4 * i + 1] = v.y, qv[4 * i + 2] = v.z, qv[4 * i + 3] = v.w;
+        }
       }
     };
-    auto store_q = [&](const uint32_t* qv, bool warp_live) {
-      if (warp_live) {
+    // ... then into TMEM (regular: the A operand of QK) or shared memory (narrow:
+    // the 128B-swizzled K-major B operand of S^T = K Q^T)
+    auto store_q = [&](uint32_t n, const uint32_t* qv) {
+      const int nr = fld(n, kFNrows);
+      if (is_narrow(n)) {
+        const int r = ln >> 3;
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+          const int ch = (ln & 7) * CPT + i, kb = ch >> 3, cc = ch & 7;
+          st_shared_v4(sQn + (uint32_t)(kb * kNarrow * 128 + r * 128 + ((cc ^ (r & 7)) << 4)),
+                       make_uint4(qv[4 * i], qv[4 * i + 1], qv[4 * i + 2], qv[4 * i + 3]));
+        }
+        fence_proxy_async_smem();
+      } else if (wq * 32 < nr) {
 #pragma unroll
         for (int i = 0; i < D / 64; ++i) tmem_st32_nowait(sp + 64u + 32u * i, qv + 32 * i);
         tmem_wait_st();
@@ -481,182 +622,340 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(QT_FULL));
     };
+    // tail of an item's span inside stage(s) from ring position g0 on: zero V rows
+    // [vt, vt rounded up to the stage) (stale / uninitialised smem; P == 0 there
+    // must not meet a NaN)
+    auto zero_v_tail = [&](int src, int s0, int vt) {
+      const int nz = (((vt + kN - 1) / kN) * kN - vt) * KB * 8;
+      for (int q = ln; q < nz; q += kM) {
+        const int rr = vt + q / (KB * 8);
+        const int kb = (q / 8) % KB, ch = q % 8;
+        st_shared_v4(sV(src, s0) + (uint32_t)(kb * L::kPlane + rr * 128 + (ch << 4)), make_uint4(0, 0, 0, 0));
+      }
+      fence_proxy_async_smem();
+    };
 
     wait_item(0);
     if (fld(0, kFIdx) >= 0) {
       uint32_t qv[D / 2];
-      const bool wl = wq * 32 < fld(0, kFNrows);
-      if (wl) load_q(0, qv);
-      store_q(qv, wl);
+      load_q(0, qv);
+      store_q(0, qv);
     }
     for (uint32_t n = 0;; ++n) {
       if (fld(n, kFIdx) < 0) break;  // ITEM_FULL(n) already waited
       const int ntok = fld(n, kFNtok);
       const int nrows = fld(n, kFNrows);
       const int src = fld(n, kFShared) ? 0 : pl;  // ring the item's tiles come from
-      const uint32_t base = src != pl ? (uint32_t)fld(n, kFG0) : rpos;
+      const uint32_t base = (uint32_t)fld(n, kFG0);
       const int kvh = fld(n, kFKvh), row0 = fld(n, kFRow0);
-      const int ntiles = (ntok + kN - 1) / kN;
-      const bool wlive = wq * 32 < nrows;  // warp has live rows (warp-uniform)
-      float m_ref = -INFINITY;             // running max, log2 units
-      float2 l2 = make_float2(0.f, 0.f);
-      bool have_next = false, next_live = false;
+      const bool narrow = is_narrow(n);
+      const int ntiles = narrow ? (ntok + kNN - 1) / kNN : (ntok + kN - 1) / kN;
+      const uint32_t meta_s = ring_s + (n & 1) * kSlotBytes + kFMeta;
+      bool have_next = false;
       uint32_t qv[D / 2];
-      long long it0 = 0, it1 = 0, it2 = 0, it3 = 0;
-      (void)it0, (void)it1, (void)it2, (void)it3;
+      long long it0 = 0, it1 = 0, it2 = 0, it3 = 0, it4 = 0, it5 = 0, it6 = 0;
+      (void)it0, (void)it1, (void)it2, (void)it3, (void)it4, (void)it5, (void)it6;
 #ifdef PAT_TC_TRACE
       if (tr) ITEM_T(it0);
 #endif
+      // next item: fetch its Q rows at the start of this item's last tile
+      // (L2-warm: the producer prefetched them at claim time)
+      auto prefetch_next_q = [&]() {
+        wait_item(n + 1);
+        have_next = fld(n + 1, kFIdx) >= 0;
+        if (have_next) load_q(n + 1, qv);
+      };
 
-      for (int t = 0; t < ntiles; ++t) {
-        const uint32_t g = tcnt + (uint32_t)t, b = g & 1;
-        if (t == ntiles - 1) {
-          // next item: fetch its Q rows now (L2-warm: the producer prefetched
-          // them at claim time) so the loads overlap this last tile
-          wait_item(n + 1);
-          have_next = fld(n + 1, kFIdx) >= 0;
-          next_live = have_next && wq * 32 < fld(n + 1, kFNrows);
-          if (next_live) load_q(n + 1, qv);
-        }
-        mbar_wait(bar(S_FULL + b), (g >> 1) & 1);
+      if (!narrow) {
+        // ================================================= regular item: thread = row
+        const bool wlive = wq * 32 < nrows;  // warp has live rows (warp-uniform)
+        float m_ref = -INFINITY;             // running max, log2 units
+        float2 l2 = make_float2(0.f, 0.f);
+        for (int t = 0; t < ntiles; ++t) {
+          const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
+          if (t == ntiles - 1) prefetch_next_q();
+          mbar_wait(bar(S_FULL + b), (c >> 1) & 1);
 #ifdef PAT_TC_TRACE
-        if (tr && t == 0) ITEM_T(it1);
-        if (tr && pl == 0) TC_TRACE(2, 0, g);
+          if (tr && t == 0) ITEM_T(it1);
+          if (tr && pl == 0) TC_TRACE(2, 0, c);
 #endif
-        tc_fence_after();
-        const uint32_t spb = sp + 32u * b;
-        if (wlive) {
-          uint32_t sr[kN];
-          tmem_ld32(spb, sr);
-          const int valid = ntok - t * kN;
-          if (valid < kN) {
+          tc_fence_after();
+          const uint32_t spb = sp + 32u * b;
+          if (wlive) {
+            uint32_t sr[kN];
+            tmem_ld32(spb, sr);
+            const int valid = ntok - t * kN;
+            if (valid < kN) {
 #pragma unroll
-            for (int k = 0; k < kN; ++k)
-              if (k >= valid) sr[k] = __float_as_uint(-INFINITY);
-          }
-          float pm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+              for (int k = 0; k < kN; ++k)
+                if (k >= valid) sr[k] = __float_as_uint(-INFINITY);
+            }
+            float pm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int k = 0; k < kN / 8; ++k)
-            pm[k & 3] = fmax3(pm[k & 3],
-                              fmax3(__uint_as_float(sr[8 * k]), __uint_as_float(sr[8 * k + 1]),
-                                    __uint_as_float(sr[8 * k + 2])),
-                              fmax3(__uint_as_float(sr[8 * k + 3]), __uint_as_float(sr[8 * k + 4]),
-                                    fmax3(__uint_as_float(sr[8 * k + 5]), __uint_as_float(sr[8 * k + 6]),
-                                          __uint_as_float(sr[8 * k + 7]))));
-          const float mx = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])) * scale_log2;
-          const bool need = mx > m_ref + kRescaleThreshold;
-          if (__any_sync(0xffffffffu, need)) {
-            const float m_new = need ? mx : m_ref;
-            const float alpha = m_new == -INFINITY ? 1.f : ex2_approx(m_ref - m_new);
-            if (t > 0) {
-              // O must hold the previous tile's PV before it is rescaled
-              const uint32_t gp = g - 1;
-              mbar_wait(bar(SP_FREE + (gp & 1)), (gp >> 1) & 1);
-              tc_fence_after();
+            for (int k = 0; k < kN / 8; ++k)
+              pm[k & 3] = fmax3(pm[k & 3],
+                                fmax3(__uint_as_float(sr[8 * k]), __uint_as_float(sr[8 * k + 1]),
+                                      __uint_as_float(sr[8 * k + 2])),
+                                fmax3(__uint_as_float(sr[8 * k + 3]), __uint_as_float(sr[8 * k + 4]),
+                                      fmax3(__uint_as_float(sr[8 * k + 5]), __uint_as_float(sr[8 * k + 6]),
+                                            __uint_as_float(sr[8 * k + 7]))));
+            const float mx = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])) * scale_log2;
+            const bool need = mx > m_ref + kRescaleThreshold;
+            if (__any_sync(0xffffffffu, need)) {
+              const float m_new = need ? mx : m_ref;
+              const float alpha = m_new == -INFINITY ? 1.f : ex2_approx(m_ref - m_new);
+              if (t > 0) {
+                // O must hold the previous tile's PV before it is rescaled
+                const uint32_t cp = c - 1;
+                mbar_wait(bar(SP_FREE + (cp & 1)), (cp >> 1) & 1);
+                tc_fence_after();
 #pragma unroll 1
-              for (int q = 0; q < D / 16; ++q) {
-                uint32_t o[16];
-                const uint32_t ta = sp + 128u + (uint32_t)(q * 16);
-                tmem_ld16(ta, o);
+                for (int q = 0; q < D / 16; ++q) {
+                  uint32_t o[16];
+                  const uint32_t ta = sp + 128u + (uint32_t)(q * 16);
+                  tmem_ld16(ta, o);
 #pragma unroll
-                for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                tmem_st16_wait(ta, o);
+                  for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                  tmem_st16_wait(ta, o);
+                }
+              }
+              l2.x *= alpha;
+              l2.y *= alpha;
+              m_ref = m_new;
+            }
+            // P = exp2(s * scale - m_ref), packed pairs (a row with no valid
+            // column so far keeps m_ref = -inf: reference 0, P = 0)
+            const float mu = m_ref == -INFINITY ? 0.f : m_ref;
+            const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mu, -mu);
+            uint32_t ph[kN / 2], plo[kN / 2];
+#pragma unroll
+            for (int k = 0; k < kN / 2; ++k) {
+              float2 a =
+                  __ffma2_rn(make_float2(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sc2, nm2);
+              a.x = ex2_approx(a.x);
+              a.y = ex2_approx(a.y);
+              ph[k] = Fmt<T>::pack(a.x, a.y);
+              if constexpr (kSplit) {
+                const float2 hf = Fmt<T>::unpack(ph[k]);
+                const float2 lo = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
+                plo[k] = Fmt<T>::pack(lo.x, lo.y);
+                l2 = __fadd2_rn(l2, a);
+              } else {
+                // normalise by the sum of the ROUNDED weights the MMA actually uses
+                l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
               }
             }
-            l2.x *= alpha;
-            l2.y *= alpha;
-            m_ref = m_new;
+            tmem_st_n<kN / 2>(spb, ph);
+            if constexpr (kSplit) tmem_st_n<kN / 2>(spb + 16u, plo);
           }
-          // P = exp2(s * scale - m_ref), packed pairs (a row with no valid
-          // column so far keeps m_ref = -inf: reference 0, P = 0)
-          const float mu = m_ref == -INFINITY ? 0.f : m_ref;
-          const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mu, -mu);
-          uint32_t ph[kN / 2], plo[kN / 2];
-#pragma unroll
-          for (int k = 0; k < kN / 2; ++k) {
-            float2 a = __ffma2_rn(make_float2(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sc2, nm2);
-            a.x = ex2_approx(a.x);
-            a.y = ex2_approx(a.y);
-            ph[k] = Fmt<T>::pack(a.x, a.y);
-            if constexpr (kSplit) {
-              const float2 hf = Fmt<T>::unpack(ph[k]);
-              const float2 lo = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
-              plo[k] = Fmt<T>::pack(lo.x, lo.y);
-              l2 = __fadd2_rn(l2, a);
-            } else {
-              // normalise by the sum of the ROUNDED weights the MMA actually uses
-              l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
-            }
-          }
-          tmem_st_n<kN / 2>(spb, ph);
-          if constexpr (kSplit) tmem_st_n<kN / 2>(spb + 16u, plo);
-        }
-        if (t * kN + kN > ntok) {
-          // tail tile: zero V rows past the span (stale / uninitialised smem,
-          // P == 0 there must not meet a NaN)
-          const int vt = ntok - t * kN;
-          const int s = (int)((base + (uint32_t)t) % kStages);
-          const int nz = (kN - vt) * KB * 8;
-          for (int q = ln; q < nz; q += kM) {
-            const int rr = vt + q / (KB * 8);
-            const int kb = (q / 8) % KB, ch = q % 8;
-            st_shared_v4(sV(src, s) + kb * (kN * 128) + rr * 128 + (ch << 4), make_uint4(0, 0, 0, 0));
-          }
-          fence_proxy_async_smem();
-        }
-        if (wlive) tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(P_FULL + b));
+          if (t * kN + kN > ntok) zero_v_tail(src, (int)((base + (uint32_t)t) % kStages), ntok - t * kN);
+          if (wlive) tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(P_FULL + b));
 #ifdef PAT_TC_TRACE
-        if (tr && pl == 0) TC_TRACE(2, 1, g);
+          if (tr && pl == 0) TC_TRACE(2, 1, c);
 #endif
-      }
+        }
 #ifdef PAT_TC_TRACE
-      if (tr) ITEM_T(it2);
+        if (tr) ITEM_T(it2);
 #endif
-      // The item's last QK completed (its S was consumed above): the next
-      // item's Q goes into TMEM now, so its first QK overlaps this epilogue.
-      if (have_next) store_q(qv, next_live);
+        // The item's last QK completed (its S was consumed above): the next
+        // item's Q goes in now, so its first QK overlaps this epilogue.
+        if (have_next) store_q(n + 1, qv);
+#ifdef PAT_TC_TRACE
+        if (tr) ITEM_T(it4);
+#endif
 
-      // ---- epilogue: the last PV of the item done -> O / l of this row
-      const uint32_t gl = tcnt + (uint32_t)ntiles - 1;
-      mbar_wait(bar(SP_FREE + (gl & 1)), (gl >> 1) & 1);
-      tc_fence_after();
-      const bool live = ln < nrows;
-      const float l = l2.x + l2.y;
-      const int2 meta = live ? lds_v2(ring_s + (n & 1) * kSlotBytes + kFMeta + 8 * ln) : make_int2(0, -1);
-      const int head = kvh * G + (live ? (row0 + ln) % G : 0);
-      if (wlive) {
-        const float inv = 1.f / l;
+        // ---- epilogue: the last PV of the item done -> O / l of this row
+        const uint32_t gl = tcnt + (uint32_t)ntiles - 1;
+        mbar_wait(bar(SP_FREE + (gl & 1)), (gl >> 1) & 1);
+#ifdef PAT_TC_TRACE
+        if (tr) ITEM_T(it5);
+#endif
+        tc_fence_after();
+        const bool live = ln < nrows;
+        const float l = l2.x + l2.y;
+        const int2 meta = live ? lds_v2(meta_s + 8 * ln) : make_int2(0, -1);
+        const int head = kvh * G + (live ? (row0 + ln) % G : 0);
+        if (wlive) {
+          // (staging O through shared memory for coalesced 128-byte row writes
+          // measured slower: c4 epilogue 5.3 -> 8.3 us per 128-row item)
+          const float inv = 1.f / l;
 #pragma unroll 1
-        for (int q = 0; q < D / 32; ++q) {
-          uint32_t o[32];
-          tmem_ld32(sp + 128u + (uint32_t)(q * 32), o);
-          if (live) {
-            const float* f = reinterpret_cast<const float*>(o);
+          for (int q = 0; q < D / 32; ++q) {
+            uint32_t o[32];
+            tmem_ld32(sp + 128u + (uint32_t)(q * 32), o);
+            if (live) {
+              const float* f = reinterpret_cast<const float*>(o);
+              if (meta.y < 0) {
+                uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)meta.x * H + head) * D + q * 32);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  dst[k] = make_uint4(Fmt<T>::pack(f[8 * k] * inv, f[8 * k + 1] * inv),
+                                      Fmt<T>::pack(f[8 * k + 2] * inv, f[8 * k + 3] * inv),
+                                      Fmt<T>::pack(f[8 * k + 4] * inv, f[8 * k + 5] * inv),
+                                      Fmt<T>::pack(f[8 * k + 6] * inv, f[8 * k + 7] * inv));
+              } else {
+                float4* dst = reinterpret_cast<float4*>(part_o + ((int64_t)meta.y * H + head) * D + q * 32);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                  dst[k] = make_float4(f[4 * k] * inv, f[4 * k + 1] * inv, f[4 * k + 2] * inv, f[4 * k + 3] * inv);
+              }
+            }
+          }
+          if (live && meta.y >= 0) part_lse[(int64_t)meta.y * H + head] = m_ref + log2f(l);
+        }
+        // O read by the lane's four warps: the next item's first PV may overwrite it
+        tc_fence_before();
+        named_bar_sync(nbar, 128);
+        if (wq == 0 && lane == 0) mbar_arrive(bar(O_EMPTY));
+      } else {
+        // ================================================= narrow item: thread = token
+        // S^T tile: lanes 0-63 = the tile's tokens (warps 0, 1), columns = the 16 rows
+        float m_ref[kNarrow], lsum[kNarrow];
+#pragma unroll
+        for (int r = 0; r < kNarrow; ++r) m_ref[r] = -INFINITY, lsum[r] = 0.f;
+        const bool tw = wq < 2;  // warp holds tokens
+        for (int t = 0; t < ntiles; ++t) {
+          const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
+          const int s0 = (int)((base + 2u * (uint32_t)t) % kStages);
+          const int vt = min(kNN, ntok - t * kNN);  // valid tokens of the tile
+          if (t == ntiles - 1) prefetch_next_q();
+          mbar_wait(bar(S_FULL + b), (c >> 1) & 1);
+#ifdef PAT_TC_TRACE
+          if (tr && t == 0) ITEM_T(it1);
+          if (tr && pl == 0) TC_TRACE(2, 0, c);
+#endif
+          tc_fence_after();
+          float x[kNarrow];
+          bool need = false;
+          if (tw) {
+            uint32_t sr[kNarrow];
+            tmem_ld16(sp + 32u * b, sr);
+            const bool tv = ln < vt;
+#pragma unroll
+            for (int r = 0; r < kNarrow; ++r) {
+              x[r] = tv && r < nrows ? __uint_as_float(sr[r]) * scale_log2 : -INFINITY;
+              need |= x[r] > m_ref[r] + kRescaleThreshold;
+            }
+          }
+          if (bar_red_or(nbar, 128, need)) {
+            // a row's max grew (always on the first tile): exact tile maxima
+            // through shared memory, O^T / sums rescaled
+            if (tw) {
+#pragma unroll
+              for (int r = 0; r < kNarrow; ++r) {
+                float v = x[r];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+                if (lane == 0) sts_f32(xch + (uint32_t)((wq * kNarrow + r) * 4), v);
+              }
+            }
+            named_bar_sync(nbar, 128);
+            float alpha[kNarrow];
+#pragma unroll
+            for (int r = 0; r < kNarrow; ++r) {
+              const float tm = fmaxf(lds_f32(xch + (uint32_t)(r * 4)), lds_f32(xch + (uint32_t)((kNarrow + r) * 4)));
+              const float mn = fmaxf(m_ref[r], tm);
+              alpha[r] = mn == -INFINITY ? 1.f : ex2_approx(m_ref[r] - mn);
+              lsum[r] *= alpha[r];
+              m_ref[r] = mn;
+            }
+            if (t > 0) {
+              // O^T must hold the previous tile's PV before it is rescaled
+              const uint32_t cp = c - 1;
+              mbar_wait(bar(SP_FREE + (cp & 1)), (cp >> 1) & 1);
+              tc_fence_after();
+              uint32_t o[kNarrow];
+              tmem_ld16(sp + 128u, o);
+#pragma unroll
+              for (int r = 0; r < kNarrow; ++r) o[r] = __float_as_uint(__uint_as_float(o[r]) * alpha[r]);
+              tmem_st16_wait(sp + 128u, o);
+            }
+            named_bar_sync(nbar, 128);  // exchange slots read before they are reused
+          }
+          if (tw) {
+            // P^T[r][token] into the K-major 128B-swizzled B operand (16 rows x 64 tokens)
+            const uint32_t toff = (uint32_t)((ln & 7) * 2);
+#pragma unroll
+            for (int r = 0; r < kNarrow; ++r) {
+              const float mu = m_ref[r] == -INFINITY ? 0.f : m_ref[r];
+              const float p = ex2_approx(x[r] - mu);
+              const uint32_t hp = Fmt<T>::pack(p, 0.f);
+              const uint32_t a = (uint32_t)(r * 128 + ((((ln >> 3) ^ (r & 7))) << 4)) + toff;
+              sts_u16(sPn(b, 0) + a, bits16(hp));
+              if constexpr (kSplit) {
+                const float hv = Fmt<T>::unpack(hp).x;
+                sts_u16(sPn(b, 1) + a, bits16(Fmt<T>::pack(p - hv, 0.f)));
+                lsum[r] += p;
+              } else {
+                lsum[r] += Fmt<T>::unpack(hp).x;
+              }
+            }
+          }
+          if (vt < kNN && (vt % kN) != 0) zero_v_tail(pl, s0, vt);
+          fence_proxy_async_smem();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(P_FULL + b));
+#ifdef PAT_TC_TRACE
+          if (tr && pl == 0) TC_TRACE(2, 1, c);
+#endif
+        }
+#ifdef PAT_TC_TRACE
+        if (tr) ITEM_T(it2);
+#endif
+        if (have_next) store_q(n + 1, qv);
+#ifdef PAT_TC_TRACE
+        if (tr) ITEM_T(it4);
+#endif
+
+        // ---- epilogue: row sums over the 64 token threads, then thread = head-dim lane
+        const uint32_t gl = tcnt + (uint32_t)ntiles - 1;
+        if (tw) {
+#pragma unroll
+          for (int r = 0; r < kNarrow; ++r) {
+            if (r >= nrows) break;
+            float v = lsum[r];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) sts_f32(xch + (uint32_t)((2 * kNarrow + wq * kNarrow + r) * 4), v);
+          }
+        }
+        mbar_wait(bar(SP_FREE + (gl & 1)), (gl >> 1) & 1);
+#ifdef PAT_TC_TRACE
+        if (tr) ITEM_T(it5);
+#endif
+        tc_fence_after();
+        uint32_t o[kNarrow];
+        tmem_ld16(sp + 128u, o);
+        tc_fence_before();
+        named_bar_sync(nbar, 128);  // sums published, O^T read by all four warps
+#ifdef PAT_TC_TRACE
+        if (tr) ITEM_T(it6);
+#endif
+        if (wq == 0 && lane == 0) mbar_arrive(bar(O_EMPTY));
+        if (ln < D) {
+          int gh = row0 % G;  // GQA head of row r within the kv head's group
+#pragma unroll
+          for (int r = 0; r < kNarrow; ++r) {
+            if (r >= nrows) break;
+            const float Ls = lds_f32(xch + (uint32_t)((2 * kNarrow + r) * 4)) +
+                             lds_f32(xch + (uint32_t)((3 * kNarrow + r) * 4));
+            const int2 meta = lds_v2(meta_s + 8 * r);
+            const int head = kvh * G + gh;
+            gh = gh + 1 == G ? 0 : gh + 1;
+            const float v = __uint_as_float(o[r]) * __frcp_rn(Ls);
             if (meta.y < 0) {
-              uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)meta.x * H + head) * D + q * 32);
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                dst[k] = make_uint4(Fmt<T>::pack(f[8 * k] * inv, f[8 * k + 1] * inv),
-                                    Fmt<T>::pack(f[8 * k + 2] * inv, f[8 * k + 3] * inv),
-                                    Fmt<T>::pack(f[8 * k + 4] * inv, f[8 * k + 5] * inv),
-                                    Fmt<T>::pack(f[8 * k + 6] * inv, f[8 * k + 7] * inv));
+              out[((int64_t)meta.x * H + head) * D + ln] = Fmt<T>::cvt(v);
             } else {
-              float4* dst = reinterpret_cast<float4*>(part_o + ((int64_t)meta.y * H + head) * D + q * 32);
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                dst[k] = make_float4(f[4 * k] * inv, f[4 * k + 1] * inv, f[4 * k + 2] * inv, f[4 * k + 3] * inv);
+              part_o[((int64_t)meta.y * H + head) * D + ln] = v;
+              if (ln == 0) part_lse[(int64_t)meta.y * H + head] = m_ref[r] + log2f(Ls);
             }
           }
         }
-        if (live && meta.y >= 0) part_lse[(int64_t)meta.y * H + head] = m_ref + log2f(l);
       }
-      // O read by the lane's four warps: the next item's first PV may overwrite it
-      tc_fence_before();
-      named_bar_sync(1 + pl, 128);
-      if (wq == 0 && lane == 0) mbar_arrive(bar(O_EMPTY));
 #ifdef PAT_TC_TRACE
       if (tr) {
         ITEM_T(it3);
@@ -664,14 +963,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (k < kItemLog) {
           long long* e = g_item_log[k];
           e[0] = blockIdx.x * 2 + pl, e[1] = fld(n, kFIdx), e[2] = nrows, e[3] = ntiles;
-          e[4] = it0, e[5] = it1, e[6] = it2, e[7] = it3;
+          e[4] = it0, e[5] = it1, e[6] = it2, e[7] = it3, e[8] = it4, e[9] = it5, e[10] = it6;
         }
       }
 #endif
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
       tcnt += (uint32_t)ntiles;
-      if (src == pl) rpos += (uint32_t)ntiles;
     }
   }
   tc_fence_before();

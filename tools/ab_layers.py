@@ -25,7 +25,8 @@ def main(names):
         q = torch.randn(w.batch, w.num_heads, w.head_dim, device="cuda", dtype=dt, generator=g)
         table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
         plan = P.PatPlan.from_table(table, w.num_heads, w.num_kv_heads, w.head_dim,
-                                    tc_min_rows=int(os.environ.get("PAT_AB_TC", "0")))
+                                    tc_min_rows=int(os.environ.get("PAT_AB_TC", "0")),
+                                    pair_items=os.environ.get("PAT_AB_PAIR") == "1")
         gr = P.PatLayerGraph(plan, q, kc, vc)
         ts = []
         for i in range(33):

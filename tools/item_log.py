@@ -34,14 +34,14 @@ def run(name, tc_min_rows=0):
     q = torch.randn(w.batch, w.num_heads, w.head_dim, device="cuda", dtype=dt, generator=g)
     table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
     plan = P.PatPlan.from_table(table, w.num_heads, w.num_kv_heads, w.head_dim, tc_min_rows=tc_min_rows,
-                                forward_only=True)
+                                forward_only=True, pair_items=os.environ.get("PAT_AB_PAIR") == "1")
     out = torch.empty_like(q)
     ws = torch.zeros(max(plan.workspace_bytes(), 256), dtype=torch.uint8, device="cuda")
     import bench
     flush = bench.L2Flush("cuda")
     lib = N.lib()
     lib.pat_debug_item_log.argtypes = [C.c_void_p, C.c_void_p]
-    log = np.zeros((32768, 8), dtype=np.int64)
+    log = np.zeros((32768, 12), dtype=np.int64)
     cnt = np.zeros(1, dtype=np.int32)
     for i in range(4):
         flush.zero_()
@@ -79,6 +79,15 @@ def run(name, tc_min_rows=0):
         nt = e[m, 3].sum()
         print(f"   {k:10s}: {m.sum():5d} items {nt:6d} tiles  {tiles[m].sum() / max(nt, 1) * 1e3:7.1f} ns/tile(in-item) "
               f" start-lat {start_lat[m].mean():.2f}  epi {epi[m].mean():.2f} us/item")
+        if e.shape[1] > 8 and (e[m, 8] > 0).all():
+            q_st = (e[m, 8] - e[m, 6]) / 1e3
+            pv = (e[m, 9] - e[m, 8]) / 1e3
+            rest = (e[m, 7] - e[m, 9]) / 1e3
+            print(f"               epilogue split: next-Q store {q_st.mean():.2f}  last-PV wait {pv.mean():.2f}  "
+                  f"O read + stores {rest.mean():.2f} us/item")
+            if (e[m, 10] > 0).all():
+                print(f"               narrow: O^T read + barrier {((e[m, 10] - e[m, 9]) / 1e3).mean():.2f}  "
+                      f"stores {((e[m, 7] - e[m, 10]) / 1e3).mean():.2f} us/item")
     worst = np.argsort(-(end - np.array([e[e[:, 0] == c, 7].max() if (e[:, 0] == c).any() else end
                                           for c in range(ncta)])))[:0]
     del worst
