@@ -62,9 +62,12 @@ enum pat_plan_flags {
   PAT_PLAN_HOST_ONLY = 1,   /* build and keep the plan on the host only (no device upload) */
   PAT_PLAN_FORWARD_ONLY = 2, /* timing aid: pat_forward launches the forward kernel(s) but not
                                the merge (multi-unit queries' outputs are left unwritten) */
-  PAT_PLAN_PAIR_ITEMS = 4    /* tcgen05: run packs wider than 128 rows as 256-row items that both
+  PAT_PLAN_PAIR_ITEMS = 4,   /* tcgen05: run packs wider than 128 rows as 256-row items that both
                                item pipelines of a CTA consume from one KV stream (half the
                                L2 -> SM bytes per row; measured neutral on c4, so opt-in) */
+  PAT_PLAN_ALL_PARTIALS = 8  /* every (unit, query) gets an fp32 partial slot (o / l, log2-sum-exp)
+                               in the workspace, even for queries covered by one unit; with
+                               FORWARD_ONLY this exposes the per-unit partials (cta_partial) */
 };
 
 typedef struct pat_plan pat_plan;

@@ -17,7 +17,12 @@ from .packer import (CtaTask, PackCache, baseline_query_centric, naive_per_node,
                      split_long_kv)
 from .plan import PatPlan
 from .attention import PatDecoder, PatLayerGraph, kv_pool_from_store, pat_attention, run_packed_attention
-from .metrics import distinct_block_census, theoretical_min_kv_bytes
+from .metrics import (TrafficReport, account_traffic, distinct_block_census, intermediate_round_trip_bytes,
+                      kv_token_bytes, theoretical_min_kv_bytes)
+from .forest import PrefixForest, PrefixNode, build_forest, flatten_forest, pack_forest, tree_heuristic
+from .numerics import (PartialBatch, PartialResult, cta_partial, dump_tensors, full_attention, gather_kv,
+                       generate_qkv, load_tensors, max_rel_error, merge_partials)
+from .schedule import TileConfig, assign_streams, plan_tasks
 from .calibration import CostModel, get_cost_model, load_profile, set_cost_model
 from .torch_op import decode_attention  # registers torch.ops.patb200.decode_attention
 

@@ -18,6 +18,7 @@ SPLIT_MODES = {"none": 0, "reference": 1, "native": 2}
 PAT_PLAN_HOST_ONLY = 1
 PAT_PLAN_FORWARD_ONLY = 2
 PAT_PLAN_PAIR_ITEMS = 4
+PAT_PLAN_ALL_PARTIALS = 8
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)

@@ -233,6 +233,7 @@ int finish_plan(pat_plan* P, const RowsView& R, int flags) {
   }
   ScheduleParams sp{P->B, P->bs, P->H, P->KVH, P->d, P->split_mode, P->num_sms, P->tc_min_rows};
   sp.pair_items = (flags & PAT_PLAN_PAIR_ITEMS) != 0;
+  sp.all_partials = (flags & PAT_PLAN_ALL_PARTIALS) != 0;
   int st = host_schedule(P->packs, sp, &P->sched);
   if (st) return st;
   P->n_slots = P->sched.n_slots;

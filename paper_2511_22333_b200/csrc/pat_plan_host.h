@@ -39,6 +39,7 @@ struct ScheduleParams {
   int B, bs, H, KVH, d, split_mode, num_sms;
   int tc_min_rows;  // rows threshold of the tcgen05 variant (0 = off)
   bool pair_items = false;  // PAT_PLAN_PAIR_ITEMS
+  bool all_partials = false;  // PAT_PLAN_ALL_PARTIALS
   pat_cost_model cm{};      // snapshot of the cost model (host_schedule takes it)
 };
 int host_schedule(const HostPacks& P, const ScheduleParams& sp, HostSchedule* out);

@@ -216,7 +216,7 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp_in, HostSchedule*
     for (int i = P.q_off[p]; i < P.q_off[p + 1]; ++i) qcnt[P.q[i]] += nparts[p];
   int32_t next = 0;
   for (int q = 0; q < sp.B; ++q) {
-    if (qcnt[q] > 1) {
+    if (qcnt[q] > 1 || (sp.all_partials && qcnt[q] > 0)) {
       S->q_slot_off[q] = next;
       S->q_nslot[q] = qcnt[q];
       next += qcnt[q];
@@ -231,7 +231,7 @@ int host_schedule(const HostPacks& P, const ScheduleParams& sp_in, HostSchedule*
     int p = S->unit_pack[u];
     for (int i = P.q_off[p]; i < P.q_off[p + 1]; ++i) {
       int q = P.q[i];
-      S->unit_slot.push_back(qcnt[q] > 1 ? S->q_slot_off[q] + qcur[q]++ : -1);
+      S->unit_slot.push_back(S->q_slot_off[q] >= 0 && qcnt[q] > 0 ? S->q_slot_off[q] + qcur[q]++ : -1);
     }
     S->unit_slot_off.push_back((int32_t)S->unit_slot.size());
   }

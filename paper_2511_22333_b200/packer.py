@@ -139,39 +139,10 @@ def split_long_kv(tasks: Sequence[CtaTask], block_size: int) -> list:
 
 
 def naive_per_node(table: BlockTable) -> Partition:
-    """PAT-naive ablation (``packer.py:171-186``): one pack per forest node.
+    """PAT-naive ablation (``packer.py:171-186``): one pack per forest node over its
+    own run, queries of its subtree, nodes in pre-order."""
+    from .forest import build_forest
 
-    Derived from the native TreeHeuristic plan's forest order is not possible
-    (merges hide nodes), so this walks the maximal-run forest directly."""
-    units = [table.row_units(q) for q in range(table.num_queries)]
-    table.validate()
-    packs = []
-
-    def node(qs, pos):
-        if len(qs) == 1:
-            tail = units[qs[0]][pos:]
-            if tail:
-                packs.append(CtaPack(tuple(qs), tuple(b for b, _ in tail), sum(t for _, t in tail)))
-            return list(qs)
-        end = pos
-        while all(end < len(units[q]) for q in qs) and len({units[q][end] for q in qs}) == 1:
-            end += 1
-        idx = len(packs)
-        packs.append(None)
-        members = [q for q in qs if len(units[q]) == end]
-        groups: dict = {}
-        for q in qs:
-            if len(units[q]) > end:
-                groups.setdefault(units[q][end], []).append(q)
-        for g in groups.values():
-            members += node(g, end)
-        run = units[qs[0]][pos:end]
-        packs[idx] = CtaPack(tuple(members), tuple(b for b, _ in run), sum(t for _, t in run))
-        return members
-
-    roots: dict = {}
-    for q in range(table.num_queries):
-        roots.setdefault(units[q][0], []).append(q)
-    for g in roots.values():
-        node(g, 0)
-    return assemble_partition([p for p in packs if p is not None], table)
+    packs = [CtaPack(tuple(n.subtree_queries()), tuple(n.block_ids), n.token_len)
+             for n in build_forest(table).iter_nodes() if n.token_len]
+    return assemble_partition(packs, table)

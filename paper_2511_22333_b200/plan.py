@@ -83,8 +83,10 @@ class PatPlan:
 
     @classmethod
     def from_units(cls, table, units, num_heads=32, num_kv_heads=8, head_dim=128, split="none", host_only=False,
-                   num_sms=0, tc_min_rows=0) -> "PatPlan":
-        """Explicit partition: ``units`` = [(query_ids, block_ids, kv_len)] in fold order."""
+                   num_sms=0, tc_min_rows=0, forward_only=False, all_partials=False) -> "PatPlan":
+        """Explicit partition: ``units`` = [(query_ids, block_ids, kv_len)] in fold order.
+        ``all_partials`` (PAT_PLAN_ALL_PARTIALS): every (unit, query) writes an fp32
+        partial to the workspace (with ``forward_only``, nothing is merged)."""
         off, blk, valid = table.csr()
         uq = [np.asarray(u[0], dtype=np.int32) for u in units]
         ub = [np.asarray(u[1], dtype=np.int32) for u in units]
@@ -95,7 +97,9 @@ class PatPlan:
         uq_all = np.concatenate(uq) if uq else np.zeros(0, np.int32)
         ub_all = np.concatenate(ub) if ub else np.zeros(0, np.int32)
         ukv = np.asarray([int(u[2]) for u in units], dtype=np.int32)
-        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms, tc_min_rows)
+        opt = cls._opts(num_heads, num_kv_heads, head_dim, split, host_only, num_sms, tc_min_rows, forward_only)
+        if all_partials:
+            opt.flags |= N.PAT_PLAN_ALL_PARTIALS
         h = C.c_void_p()
         st = N.lib().pat_plan_create_units(len(table.rows), N.ptr(off, C.c_int64), N.ptr(blk, C.c_int32),
                                            N.ptr(valid, C.c_int32), table.block_size, len(units),
