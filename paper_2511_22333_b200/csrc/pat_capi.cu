@@ -95,9 +95,13 @@ struct pat_plan {
   void* dmem = nullptr;
   DevPlan dev{};
   int device = -1;
+  // Host-side caches of pat_forward (the plan itself is immutable after
+  // creation): the fork/join streams of a multi-variant plan and the TMA
+  // descriptors of the last (k_cache, v_cache) pair, both under `mu`, so one
+  // plan may be launched from several threads / streams concurrently.
+  std::mutex mu;
   cudaStream_t streams[NUM_VARIANTS] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[NUM_VARIANTS] = {};
-  // TMA descriptors of the last (k_cache, v_cache) pair seen by pat_forward
   CUtensorMap tmk, tmv;
   const void* tm_k = nullptr;
   const void* tm_v = nullptr;
@@ -404,6 +408,8 @@ size_t pat_workspace_bytes(const pat_plan* P) {
   if (!P) return 0;
   size_t so = (size_t)P->n_slots * P->H * P->d * sizeof(float);
   size_t sl = (size_t)P->n_slots * P->H * sizeof(float);
+  // fp32 partials (o / l, log2-sum-exp), then 256 bytes of per-launch item
+  // counters (zeroed by pat_forward on the caller's stream)
   return ((so + 255) & ~size_t(255)) + ((sl + 255) & ~size_t(255)) + 256;
 }
 
@@ -442,17 +448,35 @@ int pat_forward(const pat_plan* Pc, const void* q, const void* k_cache, const vo
   int active[NUM_VARIANTS], na = 0;
   for (int v = 0; v < NUM_VARIANTS; ++v)
     if (P->items_cap[v] > 0) active[na++] = v;
-  if ((P->tm_k != k_cache || P->tm_v != v_cache || P->tm_blocks != num_pool_blocks || P->tm_dtype != dtype)) {
-    int e1 = make_kv_tensor_map(&P->tmk, k_cache, num_pool_blocks, P->bs, P->KVH, P->d, dtype);
-    int e2 = make_kv_tensor_map(&P->tmv, v_cache, num_pool_blocks, P->bs, P->KVH, P->d, dtype);
-    if (e1 || e2) {
-      set_error("cuTensorMapEncodeTiled failed (%d, %d)", e1, e2);
-      return PAT_ERR_CUDA;
+  // the dynamic item counters of this launch live in the caller's workspace:
+  // launches on different streams with different workspaces never share them
+  int32_t* sched = (int32_t*)((uint8_t*)workspace + pat_workspace_bytes(P) - 256);
+  CUDA_TRY(cudaMemsetAsync(sched, 0, 16, st));
+  CUtensorMap tmk, tmv;
+  {
+    std::lock_guard<std::mutex> lk(P->mu);
+    if ((P->tm_k != k_cache || P->tm_v != v_cache || P->tm_blocks != num_pool_blocks || P->tm_dtype != dtype)) {
+      int e1 = make_kv_tensor_map(&P->tmk, k_cache, num_pool_blocks, P->bs, P->KVH, P->d, dtype);
+      int e2 = make_kv_tensor_map(&P->tmv, v_cache, num_pool_blocks, P->bs, P->KVH, P->d, dtype);
+      if (e1 || e2) {
+        P->tm_k = nullptr;
+        set_error("cuTensorMapEncodeTiled failed (%d, %d)", e1, e2);
+        return PAT_ERR_CUDA;
+      }
+      P->tm_k = k_cache;
+      P->tm_v = v_cache;
+      P->tm_blocks = num_pool_blocks;
+      P->tm_dtype = dtype;
     }
-    P->tm_k = k_cache;
-    P->tm_v = v_cache;
-    P->tm_blocks = num_pool_blocks;
-    P->tm_dtype = dtype;
+    tmk = P->tmk;
+    tmv = P->tmv;
+    if (na > 1 && !P->ev_fork) {
+      CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+      for (int v = 0; v < NUM_VARIANTS; ++v) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&P->streams[v], cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&P->ev_join[v], cudaEventDisableTiming));
+      }
+    }
   }
   // Concurrent variants get disjoint SM shares proportional to their estimated
   // work (every forward kernel is persistent with one CTA per SM, and the
@@ -467,22 +491,16 @@ int pat_forward(const pat_plan* Pc, const void* q, const void* k_cache, const vo
   auto launch = [&](int v, cudaStream_t sv) -> cudaError_t {
     const int grid = grid_of(v);
     if (v == VAR_TC)
-      return launch_forward_tc(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2,
-                               P->dev.sched, sv);
-    return launch_forward_variant(P->tmk, P->tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sv);
+      return launch_forward_tc(tmk, tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sched, sv);
+    return launch_forward_variant(tmk, tmv, P->dev, v, grid, dtype, P->d, q, out, po, pl, scale_log2, sv);
   };
   if (na == 1) {
     CUDA_TRY(launch(active[0], st));
   } else if (na > 1) {
     // multi-stream forward (section 6): one stream per kernel config,
-    // forked from and joined back into the caller's stream.
-    if (!P->ev_fork) {
-      CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
-      for (int v = 0; v < NUM_VARIANTS; ++v) {
-        CUDA_TRY(cudaStreamCreateWithFlags(&P->streams[v], cudaStreamNonBlocking));
-        CUDA_TRY(cudaEventCreateWithFlags(&P->ev_join[v], cudaEventDisableTiming));
-      }
-    }
+    // forked from and joined back into the caller's stream (the plan's fork /
+    // join objects: concurrent multi-variant launches of ONE plan serialise on
+    // them through the stream order of their records, as CUDA events do).
     CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     for (int i = 0; i < na; ++i) {
       int v = active[i];

@@ -103,3 +103,38 @@ def test_calibrated_cost_model_plans_vs_oracle():
         plan.close()
     finally:
         CAL.set_cost_model(saved)
+
+
+def test_one_plan_two_streams_concurrently():
+    """A plan is immutable after creation: the same plan launched on two streams at
+    once (each with its own workspace and output) gives the serial result bit for
+    bit -- the dynamic item counters live in the caller's workspace."""
+    w = configs.workload("c2")
+    table = P.BlockTable([list(r) for r in w.rows], list(w.valid_last), w.block_size)
+    g = torch.Generator(device="cuda").manual_seed(21)
+    nb = w.num_pool_blocks()
+    kc = torch.randn(nb, 16, 8, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    vc = torch.randn(nb, 16, 8, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    qa = torch.randn(w.batch, 32, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    qb = torch.randn(w.batch, 32, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    plan = PatPlan.from_table(table, 32, 8, 128)
+    ref_a = P.pat_attention(plan, qa, kc, vc).clone()
+    ref_b = P.pat_attention(plan, qb, kc, vc).clone()
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    wsa = torch.empty(plan.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    wsb = torch.empty(plan.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(5):
+        oa, ob = torch.empty_like(qa), torch.empty_like(qb)
+        sa.wait_stream(torch.cuda.current_stream())
+        sb.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(sa):
+            P.pat_attention(plan, qa, kc, vc, out=oa, workspace=wsa, stream=sa)
+        with torch.cuda.stream(sb):
+            P.pat_attention(plan, qb, kc, vc, out=ob, workspace=wsb, stream=sb)
+        outs.append((oa, ob))
+    torch.cuda.synchronize()
+    for oa, ob in outs:
+        assert torch.equal(oa, ref_a) and torch.equal(ob, ref_b)
+    plan.close()
