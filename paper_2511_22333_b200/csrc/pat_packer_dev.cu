@@ -466,6 +466,8 @@ int device_pack(const int32_t* d_bt, int64_t stride, const int32_t* d_seq, int B
   cudaMemsetAsync(w.err, 0, 8, st);
   cudaMemsetAsync(w.npacks, 0, 4, st);
   cudaMemsetAsync(w.member, 0, BD1 * 4, st);
+  // node records are copied back whole; unused entries stay defined (initcheck)
+  for (int32_t* a : {w.n_rep, w.n_a0, w.n_a1, w.n_span}) cudaMemsetAsync(a, 0, N2 * 4, st);
   const int TB = 128;
   const int gq = (B + TB - 1) / TB;
   dev::k_rows<<<gq, TB, 0, st>>>(w);

@@ -1,40 +1,13 @@
 // Host C++ pack scheduler -- the paper's "async pack scheduler (C++)"
-// (PAPER.md:742), bit-exact with the reference pack_batch (packer.py:224-242).
-//
-// The algorithm is NOT the reference's recursive tree walk.  It derives the
-// whole prefix forest from the pairwise longest-common-prefix matrix of the
-// rows (as (block, tokens) units, workload.py:111-118), so that every phase is
-// a data-parallel map/reduce that the GPU packer (pat_packer_dev.cu) runs as
-// kernels; this file is the serial host driver of the same phases and is what
-// the CPU tests check against the oracle.
-//
-// For query q let D_q = sorted distinct values of lcp(q, r) >= 1 over r != q.
-//  * The internal forest nodes on q's root->leaf path end exactly at D_q
-//    (workload.py:268-273 extends a run while every member continues equally,
-//    i.e. up to the minimum lcp inside the group); level k spans
-//    [D_q[k-1], D_q[k]) and holds S_k(q) = {q} u {r : lcp(q,r) >= D_q[k]}.
-//  * If max(D_q) < len(q) (or D_q is empty) q ends in its own leaf holding the
-//    remaining suffix (workload.py:258-266); otherwise q is an empty leaf of
-//    its last internal node (workload.py:275-280).
-//  * terminal(child) (packer.py:105-110) = #members ending exactly at the
-//    child's end.
-//  * TreeHeuristic's merge rule 2*(s_c + terminal_c) > span (packer.py:153)
-//    only reads the node and its accumulated span, so each query can replay
-//    every decision on its own path independently.
-//  * q is in the pack of its path node k iff k is its last node or node k+1
-//    was split (packer.py:154-160: merged children's queries leave the
-//    parent's pack).
-//  * Children are ordered [empty leaves by qid] + [groups by min qid]
-//    (workload.py:275-294) and packs are emitted in post-order
-//    (packer.py:150-161), so the DFS rank pi(q) is the lexicographic rank of
-//    the key [min(root group), slot_0, slot_1, ...] with slot_k = q if q ends
-//    at level k else B + min(group at level k+1); packs are ordered by
-//    (last pi in the node's subtree, deeper first) and the queries inside a
-//    pack by pi.
+// (PAPER.md:742), bit-exact with the reference pack_batch (packer.py:224-242):
+// rows -> unit trie -> maximal-run prefix forest (workload.py:245-297) ->
+// TreeHeuristic packs (packer.py:124-168) -> Partition with produces_partial
+// (workload.py:377-393), linear in the number of (block, tokens) units.
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
+#include <unordered_map>
 #include <vector>
 
 #include "pat_plan_host.h"
@@ -46,17 +19,11 @@ int validate_rows(const RowsView& R) {
     set_error("block_size must be positive");
     return PAT_ERR_INVALID_SPEC;
   }
-  std::vector<int32_t> tmp;
+  int32_t maxb = -1;
   for (int q = 0; q < R.B; ++q) {
     int n = R.nblk[q];
     if (n <= 0) {
       set_error("row %d is empty", q);
-      return PAT_ERR_INVALID_SPEC;
-    }
-    tmp.assign(R.blk + R.row_begin(q), R.blk + R.row_begin(q) + n);
-    std::sort(tmp.begin(), tmp.end());
-    if (std::adjacent_find(tmp.begin(), tmp.end()) != tmp.end()) {
-      set_error("row %d repeats a block ID", q);
       return PAT_ERR_INVALID_SPEC;
     }
     int v = R.valid[q];
@@ -64,202 +31,232 @@ int validate_rows(const RowsView& R) {
       set_error("row %d valid-token count %d outside [1, block_size]", q, v);
       return PAT_ERR_INVALID_SPEC;
     }
+    for (int p = 0; p < n; ++p) {
+      const int32_t b = R.block(q, p);
+      if (b < 0) {
+        set_error("row %d has a negative block ID", q);
+        return PAT_ERR_INVALID_SPEC;
+      }
+      maxb = std::max(maxb, b);
+    }
   }
+  // a repeated block inside a row: last row that used each block id (linear)
+  std::vector<int32_t> seen((size_t)maxb + 1, -1);
+  for (int q = 0; q < R.B; ++q)
+    for (int p = 0; p < R.nblk[q]; ++p) {
+      int32_t& s = seen[R.block(q, p)];
+      if (s == q) {
+        set_error("row %d repeats a block ID", q);
+        return PAT_ERR_INVALID_SPEC;
+      }
+      s = q;
+    }
   return PAT_OK;
 }
 
-// Per-query path through the forest.
-struct QPath {
-  std::vector<int32_t> end;    // internal level ends (D_q)
-  std::vector<int32_t> nq;     // |S_k|
-  std::vector<int32_t> minq;   // min S_k
-  std::vector<int32_t> term;   // members ending exactly at end[k]
-  bool has_leaf = false;
-  // per level (internal levels, then the leaf if any)
-  std::vector<int32_t> start, stop, span, anchor;
-  std::vector<uint8_t> member;
-  int levels() const { return (int)end.size() + (has_leaf ? 1 : 0); }
+namespace {
+
+// Unit trie over the rows: node = a (block, tokens) unit at a row position;
+// children in creation order (rows inserted by query id = first appearance).
+struct TNode {
+  int32_t first_kid = -1, last_kid = -1, next_sib = -1, n_kids = 0;
+  int32_t blk = 0, tok = 0;           // the unit
+  int32_t nq = 0, first_q = -1;      // queries passing through; the smallest of them
+  int32_t ends_head = -1, ends_tail = -1, n_ends = 0;  // queries whose row ends here
+  int32_t depth = 0;                  // row position of the unit
+};
+struct UKey {
+  int32_t node, blk, tok;
+  bool operator==(const UKey& o) const { return node == o.node && blk == o.blk && tok == o.tok; }
+};
+struct UKeyHash {
+  size_t operator()(const UKey& k) const {
+    uint64_t h = (uint64_t)(uint32_t)k.node * 0x9E3779B97F4A7C15ull;
+    h ^= ((uint64_t)(uint32_t)k.blk + 0x632BE59BD9B4E019ull) * 0xC2B2AE3D27D4EB4Full;
+    h ^= (uint64_t)(uint32_t)k.tok * 0x165667B19E3779F9ull;
+    return (size_t)(h ^ (h >> 29));
+  }
 };
 
+struct TriePacker {
+  const RowsView& R;
+  std::vector<TNode> T;
+  std::vector<int32_t> next_end;  // per query: next query ending at the same trie node
+  // emitted packs: queries (flattened), rep query, [a, b) row positions, tokens
+  std::vector<int32_t> pq, pq_off{0}, prep, pa, pb, pkv;
+
+  explicit TriePacker(const RowsView& r) : R(r) {}
+
+  void build() {
+    size_t total = 0;
+    for (int q = 0; q < R.B; ++q) total += (size_t)R.nblk[q];
+    T.reserve(total + 1);
+    T.emplace_back();  // virtual root above the first units
+    // children are found by scanning the sibling list; a node whose fan-out
+    // passes kHashFrom moves its children into the hash map (a branch point
+    // of B rows costs O(B), not O(B^2))
+    constexpr int kHashFrom = 8;
+    std::unordered_map<UKey, int32_t, UKeyHash> kid;
+    next_end.assign(R.B, -1);
+    for (int q = 0; q < R.B; ++q) {
+      int32_t t = 0;
+      for (int p = 0; p < R.nblk[q]; ++p) {
+        const int32_t blk = R.block(q, p), tok = R.tokens_at(q, p);
+        int32_t c = -1;
+        if (T[t].n_kids < kHashFrom) {
+          for (int32_t k = T[t].first_kid; k >= 0; k = T[k].next_sib)
+            if (T[k].blk == blk && T[k].tok == tok) {
+              c = k;
+              break;
+            }
+        } else {
+          auto it = kid.find(UKey{t, blk, tok});
+          if (it != kid.end()) c = it->second;
+        }
+        if (c < 0) {
+          c = (int32_t)T.size();
+          T.emplace_back();
+          T[c].depth = p;
+          T[c].first_q = q;
+          T[c].blk = blk;
+          T[c].tok = tok;
+          if (T[t].last_kid < 0) T[t].first_kid = c;
+          else T[T[t].last_kid].next_sib = c;
+          T[t].last_kid = c;
+          if (++T[t].n_kids == kHashFrom)
+            for (int32_t k = T[t].first_kid; k >= 0; k = T[k].next_sib) kid.emplace(UKey{t, T[k].blk, T[k].tok}, k);
+          else if (T[t].n_kids > kHashFrom)
+            kid.emplace(UKey{t, blk, tok}, c);
+        }
+        T[c].nq++;
+        t = c;
+      }
+      if (T[t].ends_tail < 0) T[t].ends_head = q;
+      else next_end[T[t].ends_tail] = q;
+      T[t].ends_tail = q;
+      T[t].n_ends++;
+    }
+  }
+
+  // The forest node whose run starts at trie node c (workload.py:245-297): a
+  // single-query group is a leaf with the whole remaining suffix; otherwise the
+  // run extends while nobody ends and every row takes the same next unit.
+  struct FNode {
+    bool leaf;
+    int32_t q, a, b;  // rep query, run positions [a, b) of its row
+    int32_t tail;     // trie node of the run's last unit (internal nodes)
+    int32_t nq;
+    int64_t tokens;
+  };
+  FNode grow(int32_t c) const {
+    FNode f{};
+    f.q = T[c].first_q;
+    f.a = T[c].depth;
+    f.nq = T[c].nq;
+    if (T[c].nq == 1) {
+      f.leaf = true;
+      f.b = R.nblk[f.q];
+    } else {
+      int32_t t = c;
+      while (T[t].n_ends == 0 && T[t].first_kid >= 0 && T[T[t].first_kid].next_sib < 0) t = T[t].first_kid;
+      f.leaf = false;
+      f.tail = t;
+      f.b = T[t].depth + 1;
+    }
+    f.tokens = R.span_tokens(f.q, f.a, f.b);
+    return f;
+  }
+  // queries of a forest node's subtree, leaves in DFS order (empty leaves first)
+  void subtree(int32_t c, std::vector<int32_t>& out) const {
+    const FNode f = grow(c);
+    if (f.leaf) {
+      out.push_back(f.q);
+      return;
+    }
+    for (int32_t q = T[f.tail].ends_head; q >= 0; q = next_end[q]) out.push_back(q);
+    for (int32_t k = T[f.tail].first_kid; k >= 0; k = T[k].next_sib) subtree(k, out);
+  }
+  void emit(const std::vector<int32_t>& qs, int32_t rep, int32_t a, int32_t b, int64_t kv) {
+    pq.insert(pq.end(), qs.begin(), qs.end());
+    pq_off.push_back((int32_t)pq.size());
+    prep.push_back(rep);
+    pa.push_back(a);
+    pb.push_back(b);
+    pkv.push_back((int32_t)kv);
+  }
+  // TreeHeuristic (packer.py:124-161): a child is merged into the pack being
+  // built iff 2 (s_child + terminal_child) > span; children's packs come first.
+  void visit(int32_t c, bool inherit, int32_t anchor, int64_t span_in) {
+    const FNode f = grow(c);
+    const int32_t a = inherit ? anchor : f.a;
+    const int64_t span = (inherit ? span_in : 0) + f.tokens;
+    if (f.leaf) {
+      if (span > 0) emit({f.q}, f.q, a, f.b, span);
+      return;
+    }
+    std::vector<int32_t> rest;
+    for (int32_t q = T[f.tail].ends_head; q >= 0; q = next_end[q]) rest.push_back(q);
+    for (int32_t k = T[f.tail].first_kid; k >= 0; k = T[k].next_sib) {
+      const FNode g = grow(k);
+      const int32_t terminal = g.leaf ? 1 : T[g.tail].n_ends;
+      if (2 * (int64_t)(g.nq + terminal) > span) {
+        visit(k, true, a, span);  // merged: its queries leave this pack
+      } else {
+        visit(k, false, 0, 0);
+        subtree(k, rest);
+      }
+    }
+    if (!rest.empty() && span > 0) emit(rest, f.q, a, f.b, span);
+  }
+};
+
+}  // namespace
+
+// Linear in the table size: a unit trie (hash map keyed by (node, block,
+// tokens)), compressed into the maximal-run forest on the fly, with the
+// TreeHeuristic emitting packs in post-order.  (The GPU pass in
+// pat_packer_dev.cu derives the same partition from pairwise prefixes.)
 int host_pack(const RowsView& R, HostPacks* out) {
   const int B = R.B;
   out->clear();
   if (B == 0) return PAT_OK;
   int st = validate_rows(R);
   if (st) return st;
-
-  // Phase 1: pairwise lcp over units.
-  std::vector<int32_t> lcp((size_t)B * B);
-  for (int q = 0; q < B; ++q) {
-    lcp[(size_t)q * B + q] = R.nblk[q];
-    for (int r = q + 1; r < B; ++r) {
-      int n = std::min(R.nblk[q], R.nblk[r]);
-      int p = 0;
-      while (p < n && R.same_unit(q, r, p)) ++p;
-      lcp[(size_t)q * B + r] = lcp[(size_t)r * B + q] = p;
-    }
-  }
-
-  // Phase 2: per-query levels.
-  std::vector<QPath> P(B);
-  std::vector<int32_t> vals;
-  for (int q = 0; q < B; ++q) {
-    QPath& qp = P[q];
-    const int32_t* L = &lcp[(size_t)q * B];
-    vals.clear();
-    for (int r = 0; r < B; ++r)
-      if (r != q && L[r] >= 1) vals.push_back(L[r]);
-    std::sort(vals.begin(), vals.end());
-    vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
-    qp.end = vals;
-    const int K = (int)vals.size();
-    qp.nq.assign(K, 1);
-    qp.minq.assign(K, q);
-    qp.term.assign(K, 0);
-    for (int k = 0; k < K; ++k) {
-      int e = vals[k];
-      if (R.nblk[q] == e) qp.term[k] += 1;
-      for (int r = 0; r < B; ++r) {
-        if (r == q || L[r] < e) continue;
-        qp.nq[k] += 1;
-        qp.minq[k] = std::min(qp.minq[k], r);
-        if (L[r] == e && R.nblk[r] == e) qp.term[k] += 1;
-      }
-    }
-    qp.has_leaf = (K == 0) || vals[K - 1] < R.nblk[q];
-  }
-
-  // Phase 3: replay TreeHeuristic decisions along each path.
-  std::vector<int32_t> nmemb(B, 0);
-  for (int q = 0; q < B; ++q) {
-    QPath& qp = P[q];
-    const int K = (int)qp.end.size();
-    const int Lv = qp.levels();
-    qp.start.resize(Lv);
-    qp.stop.resize(Lv);
-    qp.span.resize(Lv);
-    qp.anchor.resize(Lv);
-    qp.member.assign(Lv, 0);
-    std::vector<uint8_t> merged(Lv, 0);
-    for (int k = 0; k < Lv; ++k) {
-      qp.start[k] = k == 0 ? 0 : qp.end[k - 1];
-      qp.stop[k] = k < K ? qp.end[k] : R.nblk[q];
-      int64_t tok = R.span_tokens(q, qp.start[k], qp.stop[k]);
-      if (k == 0) {
-        qp.span[k] = (int32_t)tok;
-        qp.anchor[k] = 0;
-      } else {
-        int s_c = k < K ? qp.nq[k] : 1;
-        int t_c = k < K ? qp.term[k] : 1;
-        merged[k] = 2 * (int64_t)(s_c + t_c) > qp.span[k - 1];
-        qp.span[k] = merged[k] ? qp.span[k - 1] + (int32_t)tok : (int32_t)tok;
-        qp.anchor[k] = merged[k] ? qp.anchor[k - 1] : qp.start[k];
-      }
-    }
-    for (int k = 0; k < Lv; ++k) {
-      qp.member[k] = (k == Lv - 1) || !merged[k + 1];
-      nmemb[q] += qp.member[k];
-    }
-  }
-
-  // Phase 4: DFS rank pi(q) = lexicographic rank of the child-slot key.
-  std::vector<std::vector<int32_t>> key(B);
-  for (int q = 0; q < B; ++q) {
-    const QPath& qp = P[q];
-    const int K = (int)qp.end.size();
-    key[q].push_back(K > 0 ? qp.minq[0] : q);
-    for (int k = 0; k < K; ++k) {
-      if (qp.end[k] == R.nblk[q]) key[q].push_back(q);
-      else key[q].push_back(B + (k + 1 < K ? qp.minq[k + 1] : q));
-    }
-  }
-  std::vector<int32_t> order(B);
-  std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](int a, int b) { return key[a] < key[b]; });
-  std::vector<int32_t> pi(B);
-  for (int i = 0; i < B; ++i) pi[order[i]] = i;
-
-  // Phase 5: nodes.  Node (owner m, level k) where owner = min of the level's set
-  // (the query itself at its leaf).  m owns a contiguous suffix of its levels.
-  auto owner = [&](int q, int k) { return k < (int)P[q].end.size() ? P[q].minq[k] : q; };
-  std::vector<int32_t> k0(B), base(B + 1, 0);
-  for (int m = 0; m < B; ++m) {
-    int Lv = P[m].levels(), k = 0;
-    while (k < Lv && owner(m, k) != m) ++k;
-    k0[m] = k;
-    base[m + 1] = base[m] + (Lv - k);
-  }
-  const int N = base[B];
-  std::vector<int32_t> hi(N, 0), cnt(N, 0), depth(N), rep(N), a0(N), a1(N), span(N);
-  for (int m = 0; m < B; ++m)
-    for (int k = k0[m]; k < P[m].levels(); ++k) {
-      int id = base[m] + k - k0[m];
-      depth[id] = k;
-      rep[id] = m;
-      a0[id] = P[m].anchor[k];
-      a1[id] = P[m].stop[k];
-      span[id] = P[m].span[k];
-    }
-  for (int q = 0; q < B; ++q)
-    for (int k = 0; k < P[q].levels(); ++k) {
-      int m = owner(q, k);
-      int id = base[m] + k - k0[m];
-      hi[id] = std::max(hi[id], pi[q] + 1);
-      cnt[id] += P[q].member[k];
-    }
-
-  // Phase 6: emission order = (hi ascending, deeper first); queries by pi.
-  std::vector<int32_t> nodes;
-  for (int i = 0; i < N; ++i)
-    if (cnt[i] > 0) nodes.push_back(i);
-  std::sort(nodes.begin(), nodes.end(), [&](int a, int b) {
-    return hi[a] != hi[b] ? hi[a] < hi[b] : depth[a] > depth[b];
-  });
-  std::vector<int32_t> pack_of(N, -1);
-  for (size_t i = 0; i < nodes.size(); ++i) pack_of[nodes[i]] = (int)i;
-  const int NP = (int)nodes.size();
-  out->q_off.assign(NP + 1, 0);
-  out->blk_off.assign(NP + 1, 0);
-  out->kv.resize(NP);
-  out->partial.assign(NP, 0);
-  out->rep.resize(NP);
-  out->blk_begin.resize(NP);
+  TriePacker tp(R);
+  tp.build();
+  for (int32_t k = tp.T[0].first_kid; k >= 0; k = tp.T[k].next_sib) tp.visit(k, false, 0, 0);
+  const int NP = (int)tp.pkv.size();
+  std::vector<int32_t> cnt(B, 0);
+  for (int32_t q : tp.pq) cnt[q]++;
+  out->q = tp.pq;
+  out->q_off = tp.pq_off;
+  out->blk_off.assign(1, 0);
   for (int p = 0; p < NP; ++p) {
-    int id = nodes[p];
-    out->q_off[p + 1] = out->q_off[p] + cnt[id];
-    out->blk_off[p + 1] = out->blk_off[p] + (a1[id] - a0[id]);
-    out->kv[p] = span[id];
-    out->rep[p] = rep[id];
-    out->blk_begin[p] = a0[id];
-  }
-  out->q.assign(out->q_off[NP], -1);
-  out->blk.resize(out->blk_off[NP]);
-  std::vector<int32_t> cursor(out->q_off.begin(), out->q_off.end() - 1);
-  for (int i = 0; i < B; ++i) {
-    int q = order[i];
-    for (int k = 0; k < P[q].levels(); ++k) {
-      if (!P[q].member[k]) continue;
-      int m = owner(q, k);
-      int p = pack_of[base[m] + k - k0[m]];
-      out->q[cursor[p]++] = q;
-      if (nmemb[q] > 1) out->partial[p] = 1;
-    }
-  }
-  for (int p = 0; p < NP; ++p) {
-    int id = nodes[p];
-    for (int j = a0[id]; j < a1[id]; ++j) out->blk[out->blk_off[p] + j - a0[id]] = R.block(rep[id], j);
+    uint8_t part = 0;
+    for (int i = tp.pq_off[p]; i < tp.pq_off[p + 1]; ++i) part |= cnt[tp.pq[i]] > 1;
+    out->partial.push_back(part);
+    out->kv.push_back(tp.pkv[p]);
+    out->rep.push_back(tp.prep[p]);
+    out->blk_begin.push_back(tp.pa[p]);
+    for (int j = tp.pa[p]; j < tp.pb[p]; ++j) out->blk.push_back(R.block(tp.prep[p], j));
+    out->blk_off.push_back((int32_t)out->blk.size());
   }
   return PAT_OK;
 }
 
 int64_t distinct_tokens(const RowsView& R) {
-  std::vector<std::pair<int32_t, int32_t>> u;
+  // fullest use of every block id (simulator.py:68-75), one pass
+  int32_t maxb = -1;
   for (int q = 0; q < R.B; ++q)
-    for (int p = 0; p < R.nblk[q]; ++p) u.emplace_back(R.block(q, p), R.tokens_at(q, p));
-  std::sort(u.begin(), u.end());
+    for (int p = 0; p < R.nblk[q]; ++p) maxb = std::max(maxb, R.block(q, p));
+  std::vector<int32_t> best((size_t)maxb + 1, 0);
+  for (int q = 0; q < R.B; ++q)
+    for (int p = 0; p < R.nblk[q]; ++p) {
+      int32_t& b = best[R.block(q, p)];
+      b = std::max(b, R.tokens_at(q, p));
+    }
   int64_t tot = 0;
-  for (size_t i = 0; i < u.size(); ++i)
-    if (i + 1 == u.size() || u[i + 1].first != u[i].first) tot += u[i].second;  // max fill per block
+  for (int32_t t : best) tot += t;
   return tot;
 }
 
