@@ -176,6 +176,34 @@ int pat_forward(const pat_plan* plan, const void* q, const void* k_cache, const 
 
 void pat_plan_destroy(pat_plan* plan);
 
+/* ---------------------------------------------------------------------------------
+ * Device-resident decoder: the serving path with planning on the GPU.
+ * Replaces packer.py:189-266 (PackCache + pack_batch_async) and the per-step
+ * pack_batch -> run_packed_attention of a serving engine.
+ * pat_decoder_forward enqueues on `stream`, with no host synchronisation and no
+ * allocation: a 64-bit fingerprint of (block_tables, seq_lens), a comparison with
+ * the last one on the device, the GPU packer and the device scheduler (both skip
+ * at once when the table is unchanged), then the forward and merge kernels over
+ * the device plan.  A CUDA graph of it stays valid while the table contents change.
+ * max_batch <= 4096; a table outside the decoder's capacity is rejected.  An
+ * invalid table (empty row, repeated block) makes the step a no-op on the device;
+ * pat_decoder_status (synchronising) reports it and the re-plan count. */
+typedef struct pat_decoder pat_decoder;
+enum pat_decode_flags {
+  PAT_DECODE_SAME_TABLE = 1  /* the caller guarantees the table is the one of the previous call
+                               (e.g. the other layers of a decode step): forward + merge only */
+};
+int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t max_blocks,
+                       int32_t block_size, pat_decoder** out);
+size_t pat_decoder_workspace_bytes(const pat_decoder* dec);
+int pat_decoder_forward(pat_decoder* dec, const int32_t* block_tables, int64_t bt_stride,
+                        const int32_t* seq_lens, int32_t B, int32_t max_blocks, const void* q,
+                        const void* k_cache, const void* v_cache, int64_t num_pool_blocks, void* out,
+                        void* workspace, size_t workspace_bytes, int32_t dtype, float scale,
+                        int32_t flags, void* stream);
+int pat_decoder_status(pat_decoder* dec, void* stream, int32_t* replans);
+void pat_decoder_destroy(pat_decoder* dec);
+
 const char* pat_last_error(void);
 
 /* Library version string. */

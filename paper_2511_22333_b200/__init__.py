@@ -16,7 +16,7 @@ from .workload import (BlockTable, CtaPack, Partition, WorkloadSpec, assemble_pa
 from .packer import (CtaTask, PackCache, baseline_query_centric, naive_per_node, pack_batch, pack_batch_async,
                      split_long_kv)
 from .plan import PatPlan
-from .attention import PatDecoder, PatLayerGraph, kv_pool_from_store, pat_attention, run_packed_attention
+from .attention import PatDecoder, PatDeviceDecoder, PatLayerGraph, kv_pool_from_store, pat_attention, run_packed_attention
 from .metrics import (TrafficReport, account_traffic, distinct_block_census, intermediate_round_trip_bytes,
                       kv_token_bytes, theoretical_min_kv_bytes)
 from .forest import PrefixForest, PrefixNode, build_forest, flatten_forest, pack_forest, tree_heuristic

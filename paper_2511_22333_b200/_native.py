@@ -19,6 +19,7 @@ PAT_PLAN_HOST_ONLY = 1
 PAT_PLAN_FORWARD_ONLY = 2
 PAT_PLAN_PAIR_ITEMS = 4
 PAT_PLAN_ALL_PARTIALS = 8
+PAT_DECODE_SAME_TABLE = 1
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)
@@ -63,6 +64,14 @@ SIGNATURES = [
     ("pat_forward", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                               C.c_size_t, C.c_int32, C.c_float, C.c_void_p]),
     ("pat_plan_destroy", None, [C.c_void_p]),
+    ("pat_decoder_create", C.c_int, [C.POINTER(PlanOptions), C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(C.c_void_p)]),
+    ("pat_decoder_workspace_bytes", C.c_size_t, [C.c_void_p]),
+    ("pat_decoder_forward", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                      C.c_size_t, C.c_int32, C.c_float, C.c_int32, C.c_void_p]),
+    ("pat_decoder_status", C.c_int, [C.c_void_p, C.c_void_p, i32p]),
+    ("pat_decoder_destroy", None, [C.c_void_p]),
     ("pat_last_error", C.c_char_p, []),
     ("pat_version", C.c_char_p, []),
 ]

@@ -157,6 +157,99 @@ class PatDecoder:
         return pat_attention(plan, q, k_cache, v_cache, out=out, workspace=self.workspace(plan), scale=scale)
 
 
+class PatDeviceDecoder:
+    """Serving path with planning on the GPU (``pat_decoder``, ``include/pat.h``).
+
+    ``forward(block_tables, seq_lens, q, k_cache, v_cache)`` enqueues the table
+    fingerprint, its comparison with the last one, the GPU packer and the device
+    scheduler (skipped on the device when the table is unchanged) and the
+    forward + merge kernels -- no host synchronisation, no allocation -- so a
+    decode step can be captured in a CUDA graph once and replayed while vLLM
+    rewrites its block table in place.  Capacity: ``max_batch`` <= 4096 queries
+    of <= ``max_blocks`` pages."""
+
+    def __init__(self, num_heads: int, num_kv_heads: int, head_dim: int, max_batch: int, max_blocks: int,
+                 block_size: int = 16, device: Union[str, torch.device] = "cuda"):
+        self.num_heads, self.num_kv_heads, self.head_dim = num_heads, num_kv_heads, head_dim
+        self.max_batch, self.max_blocks, self.block_size = max_batch, max_blocks, block_size
+        self.device = torch.device(device)
+        opt = PatPlan._opts(num_heads, num_kv_heads, head_dim, "native", False)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            N.check(N.lib().pat_decoder_create(C.byref(opt), max_batch, max_blocks, block_size, C.byref(h)),
+                    "pat_decoder_create")
+        self._h = h
+        need = int(N.lib().pat_decoder_workspace_bytes(h))
+        self.workspace = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        self._last_table = None
+
+    def fits(self, block_tables) -> bool:
+        return block_tables.shape[0] <= self.max_batch and block_tables.shape[1] <= self.max_blocks
+
+    def forward(self, block_tables, seq_lens, q, k_cache, v_cache, out=None, scale=None, stream=None):
+        """Every layer of a decode step passes the same (unmodified) table tensors:
+        those calls skip even the device fingerprint (tensor identity + autograd
+        version counter, the PAT_DECODE_SAME_TABLE flag)."""
+        if q.dtype not in _DTYPES or k_cache.dtype != q.dtype or v_cache.dtype != q.dtype:
+            raise ShapeMismatch("q, k_cache, v_cache must share dtype float16 or bfloat16")
+        if q.dim() != 3 or q.shape[1] != self.num_heads or q.shape[2] != self.head_dim:
+            raise ShapeMismatch(f"q must be [B, {self.num_heads}, {self.head_dim}], got {tuple(q.shape)}")
+        if block_tables.dim() != 2 or block_tables.shape[0] != q.shape[0] or seq_lens.shape[0] != q.shape[0]:
+            raise ShapeMismatch("Q row count must match the table")
+        if block_tables.dtype != torch.int32 or seq_lens.dtype != torch.int32 or block_tables.stride(1) != 1:
+            raise ShapeMismatch("block_tables / seq_lens must be int32 with unit column stride")
+        if k_cache.shape != v_cache.shape or k_cache.dim() != 4 or k_cache.shape[1] != self.block_size \
+                or k_cache.shape[2] != self.num_kv_heads or k_cache.shape[3] != self.head_dim:
+            raise ShapeMismatch("k_cache/v_cache must be [num_blocks, page, KVH, d]")
+        if not (q.is_contiguous() and k_cache.is_contiguous() and v_cache.is_contiguous()
+                and seq_lens.is_contiguous()):
+            raise ShapeMismatch("tensors must be contiguous")
+        if out is None:
+            out = torch.empty_like(q)
+        elif out.shape != q.shape or out.dtype != q.dtype or not out.is_contiguous():
+            raise ShapeMismatch("out must be a contiguous tensor with q's shape and dtype")
+        s = stream if stream is not None else torch.cuda.current_stream(q.device)
+        # the identity shortcut is only sound while every plan change goes through
+        # these calls: once the decoder has been captured in a CUDA graph (whose
+        # replays re-plan on the device, invisibly to this object) it is not used
+        # again; inside one capture it still applies from the second call on
+        capturing = torch.cuda.is_current_stream_capturing()
+        if capturing and not getattr(self, "_capturing", False):
+            self._last_table = None
+        self._capturing = capturing
+        self._captured = getattr(self, "_captured", False) or capturing
+        ident = (block_tables.data_ptr(), block_tables._version, tuple(block_tables.shape), block_tables.stride(0),
+                 seq_lens.data_ptr(), seq_lens._version)
+        flags = N.PAT_DECODE_SAME_TABLE if (ident == self._last_table and (capturing or not self._captured)) else 0
+        N.check(N.lib().pat_decoder_forward(
+            self._h, C.c_void_p(block_tables.data_ptr()), block_tables.stride(0), C.c_void_p(seq_lens.data_ptr()),
+            q.shape[0], block_tables.shape[1], C.c_void_p(q.data_ptr()), C.c_void_p(k_cache.data_ptr()),
+            C.c_void_p(v_cache.data_ptr()), k_cache.shape[0], C.c_void_p(out.data_ptr()),
+            C.c_void_p(self.workspace.data_ptr()), self.workspace.numel(), _DTYPES[q.dtype],
+            float(scale) if scale else 0.0, flags, C.c_void_p(s.cuda_stream)), "pat_decoder_forward")
+        self._last_table = ident
+        return out
+
+    def status(self, stream=None) -> int:
+        """Synchronise; raise the packer's error for the last table (InvalidSpec, ...);
+        return how many times the device re-planned."""
+        n = C.c_int32(0)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        N.check(N.lib().pat_decoder_status(self._h, C.c_void_p(s.cuda_stream), C.byref(n)), "pat_decoder")
+        return int(n.value)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().pat_decoder_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class PatLayerGraph:
     """One decode-attention layer captured as a CUDA graph (the multi-stream
     fork/join inside ``pat_forward`` is captured too); ``replay()`` re-runs it on

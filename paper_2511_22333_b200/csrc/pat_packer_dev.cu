@@ -16,8 +16,13 @@
 // Output (device): packs as (rep query, first block, end block, kv_len,
 // query list, partial) in reference order; bit-exact with pack_batch.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <mutex>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "pat_plan_host.h"
 
@@ -30,6 +35,7 @@ struct Ws {
   int64_t stride;
   const int32_t* seq;
   int B, bs, maxb, D;  // D = level capacity per query
+  const int32_t* run;  // device flag: the table changed, re-plan (nullptr = always run)
   // per query
   int32_t* nblk;
   int32_t* valid;
@@ -74,6 +80,7 @@ __device__ __forceinline__ int tok_at(const Ws& w, int q, int p) { return p == w
 __device__ __forceinline__ int blk_at(const Ws& w, int q, int p) { return w.bt[(int64_t)q * w.stride + p]; }
 
 __global__ void k_rows(Ws w) {
+  if (w.run && !*w.run) return;
   int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= w.B) return;
   int s = w.seq[q];
@@ -87,6 +94,7 @@ __global__ void k_rows(Ws w) {
 
 // one CTA per row: bitonic sort of the row's block ids in smem, adjacent compare
 __global__ void k_dup(Ws w) {
+  if (w.run && !*w.run) return;
   extern __shared__ int32_t sbuf[];
   const int q = blockIdx.x;
   const int n = min(w.nblk[q], w.maxb);
@@ -118,6 +126,7 @@ __global__ void k_dup(Ws w) {
 
 // one warp per (q, r) pair with q < r
 __global__ void k_lcp(Ws w) {
+  if (w.run && !*w.run) return;
   const int lane = threadIdx.x & 31;
   const int64_t npairs = (int64_t)w.B * w.B;
   for (int64_t pr = (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) / 32; pr < npairs;
@@ -146,6 +155,7 @@ __global__ void k_lcp(Ws w) {
 
 // one CTA per query: sort (lcp, r) keys, derive the internal levels
 __global__ void k_levels(Ws w) {
+  if (w.run && !*w.run) return;
   extern __shared__ unsigned long long skey[];
   const int q = blockIdx.x;
   int P = 1;
@@ -228,6 +238,7 @@ __device__ __forceinline__ int64_t span_tokens(const Ws& w, int q, int a, int b)
 
 // thread per query: TreeHeuristic decisions along the path + ownership
 __global__ void k_decide(Ws w) {
+  if (w.run && !*w.run) return;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= w.B) return;
   const int K = w.K[q], Lv = levels_of(w, q), D1 = w.D + 1;
@@ -273,6 +284,7 @@ __device__ __forceinline__ int key_at(const Ws& w, int q, int e) {
 
 // warp per query: pi(q) = #{r : key(r) < key(q)}
 __global__ void k_rank(Ws w) {
+  if (w.run && !*w.run) return;
   const int q = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (q >= w.B) return;
   const int lq = w.K[q] + 1;
@@ -304,6 +316,7 @@ __global__ void k_rank(Ws w) {
 
 // single CTA exclusive scan of cnt_own -> base
 __global__ void k_scan_nodes(Ws w) {
+  if (w.run && !*w.run) return;
   __shared__ int32_t part[1024];
   const int t = threadIdx.x, n = w.B;
   const int per = (n + blockDim.x - 1) / blockDim.x;
@@ -334,6 +347,7 @@ __device__ __forceinline__ int node_id(const Ws& w, int q, int k) {
 }
 
 __global__ void k_nodes_init(Ws w) {
+  if (w.run && !*w.run) return;
   const int N = w.base[w.B];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     w.n_hi[i] = 0;
@@ -345,6 +359,7 @@ __global__ void k_nodes_init(Ws w) {
 
 // thread per query: every level it passes through
 __global__ void k_nodes(Ws w) {
+  if (w.run && !*w.run) return;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= w.B) return;
   const int Lv = levels_of(w, q), D1 = w.D + 1;
@@ -366,6 +381,7 @@ __global__ void k_nodes(Ws w) {
 
 // thread per node: rank among emitting nodes by (hi asc, depth desc)
 __global__ void k_order(Ws w) {
+  if (w.run && !*w.run) return;
   const int N = w.base[w.B];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     if (w.n_cnt[i] == 0) continue;
@@ -384,6 +400,7 @@ __global__ void k_order(Ws w) {
 
 // single thread: query offsets per pack (packs <= 2B)
 __global__ void k_pack_offsets(Ws w) {
+  if (w.run && !*w.run) return;
   const int np = *w.npacks;
   int acc = 0;
   for (int p = 0; p < np; ++p) {
@@ -396,6 +413,7 @@ __global__ void k_pack_offsets(Ws w) {
 
 // thread per query: place it in each pack it belongs to, in pi order
 __global__ void k_members(Ws w) {
+  if (w.run && !*w.run) return;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= w.B) return;
   const int Lv = levels_of(w, q), D1 = w.D + 1;
@@ -610,4 +628,633 @@ extern "C" int pat_table_hash_device(int32_t B, const int32_t* block_tables, int
     return PAT_ERR_CUDA;
   }
   return PAT_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// Device-resident planner (pat_decoder): fingerprint -> compare -> GPU packer ->
+// on-device schedule -> forward + merge, all stream-ordered with no host
+// synchronisation and no allocation, so a serving step (or a CUDA graph of it)
+// re-plans only when the block table changed (packer.py:189-221 lazy update,
+// PAPER.md:433 "scheduler run asynchronously").
+// ------------------------------------------------------------------------------------------
+namespace pat {
+
+cudaError_t launch_forward_tc(const CUtensorMap& tmk, const CUtensorMap& tmv, const DevPlan& plan, int var, int grid,
+                              int dtype, int d, const void* q, void* out, float* po, float* pl, float scale_log2,
+                              int32_t* sched, cudaStream_t st);
+cudaError_t launch_merge(const DevPlan& plan, int grid, int dtype, int d, const float* po, const float* pl, void* out,
+                         cudaStream_t st);
+int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t num_blocks, int bs, int kvh, int d, int dtype);
+
+namespace dev {
+
+__global__ void k_reset(Ws w, int N2) {
+  if (w.run && !*w.run) return;
+  const int BD1 = w.B * (w.D + 1);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < BD1; i += gridDim.x * blockDim.x) w.member[i] = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N2; i += gridDim.x * blockDim.x)
+    w.n_rep[i] = w.n_a0[i] = w.n_a1[i] = w.n_span[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.err[0] = w.err[1] = *w.npacks = 0;
+}
+
+// table fingerprint seed, then compare with the last one: run = changed
+__global__ void k_hash_seed(unsigned long long* h, int B, int bs) {
+  *h = ((unsigned long long)(unsigned)B << 32) ^ (unsigned long long)(unsigned)bs ^ 0x7A7A000000000000ull;
+}
+__global__ void k_hash_check(const unsigned long long* h_new, unsigned long long* h_old, int32_t* run, int32_t* nrun) {
+  const bool changed = *h_new != *h_old;
+  *run = changed ? 1 : 0;
+  if (changed) {
+    *h_old = *h_new;
+    atomicAdd(nrun, 1);
+  }
+}
+
+struct Sched {
+  Ws w;
+  // outputs (the DevPlan points at these)
+  int32_t* pack_blk_off;  // [2B+2]
+  int32_t* pack_blk;      // [cap_blk]
+  int32_t* unit_pack;     // [cap_units]
+  int32_t* unit_page0;
+  int32_t* unit_ntok;
+  int32_t* unit_slot_off; // [cap_units+1]
+  int32_t* unit_slot;     // [cap_members]
+  Item* items;            // [cap_items]
+  int32_t* n_items;       // [NUM_VARIANTS]
+  int32_t* n_pair;        // [NUM_VARIANTS]
+  int4* merge_desc;       // [B]
+  int32_t* n_merge;       // [1]
+  // scratch
+  int32_t* parts;         // [2B+2]
+  int32_t* ubase;         // [2B+3]
+  int32_t* qcnt;          // [B]
+  int32_t* qoff;          // [B]
+  int32_t* qlist_n;       // [B]
+  int2* qlist;            // [B][D+1] (pack, member index)
+  int32_t* prior;         // [pack members] units of the member's query in earlier packs
+  unsigned long long* ukey;  // [cap_units] sort keys
+  // capacities
+  int cap_blk, cap_units, cap_members, cap_items, cap_slots;
+  // model
+  float item_ns, row_ns, step_ns, hbm_bpns;
+  int lanes, H, KVH, d, G;
+};
+
+// exclusive scan over n values produced by `val(i)` with one CTA; returns the total
+template <typename F, typename O>
+__device__ int cta_scan(int n, F val, O put) {
+  __shared__ int part[1024];
+  __shared__ int total;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
+  int s = 0;
+  for (int i = t * per; i < min(n, (t + 1) * per); ++i) s += val(i);
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int acc = 0;
+    for (int i = 0; i < nt; ++i) {
+      const int v = part[i];
+      part[i] = acc;
+      acc += v;
+    }
+    total = acc;
+  }
+  __syncthreads();
+  int acc = part[t];
+  for (int i = t * per; i < min(n, (t + 1) * per); ++i) {
+    put(i, acc);
+    acc += val(i);
+  }
+  __syncthreads();
+  const int r = total;
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ float sched_item_ns(const Sched& S, int rows, int ntok) {
+  const float steps = (float)((ntok + 63) / 64);
+  return S.item_ns + S.row_ns * rows / 128.f + steps * S.step_ns * (0.5f + 0.5f * S.d / 128.f);
+}
+
+// One CTA: split (chunk chosen by a makespan estimate over the lanes), units,
+// partial slots in unit order, longest-first work items, merge descriptors.
+__global__ void __launch_bounds__(1024) k_schedule(Sched S) {
+  const Ws& w = S.w;
+  if (w.run && !*w.run) return;
+  const int t = threadIdx.x, nt = blockDim.x;
+  __shared__ int s_np, s_err, s_chunk;
+  __shared__ float s_best[32];
+  if (t == 0) {
+    s_np = *w.npacks;
+    s_err = w.err[0];
+  }
+  __syncthreads();
+  const int NP = s_np;
+  if (s_err || NP == 0) {  // invalid table: nothing runs (pat_decoder_status reports it)
+    if (t < NUM_VARIANTS) S.n_items[t] = S.n_pair[t] = 0;
+    if (t == 0) *S.n_merge = 0;
+    return;
+  }
+  auto pk_node = [&](int p) { return w.p_node[p]; };
+  auto pk_pages = [&](int p) { const int id = pk_node(p); return w.n_a1[id] - w.n_a0[id]; };
+  auto pk_rows = [&](int p) { return (w.p_qoff[p + 1] - w.p_qoff[p]) * S.G; };
+  auto pk_kv = [&](int p) { return w.n_span[pk_node(p)]; };
+
+  // pack spans: the rep query's row [a0, a1)
+  const int nblk = cta_scan(NP, pk_pages, [&](int i, int v) { S.pack_blk_off[i] = v; });
+  if (t == 0) S.pack_blk_off[NP] = nblk;
+  const int wp = t >> 5, ln = t & 31, nwp = nt >> 5;  // warp per pack / unit below
+  for (int p = wp; p < NP; p += nwp) {
+    const int id = pk_node(p), rep = w.n_rep[id], a0 = w.n_a0[id], n = w.n_a1[id] - a0;
+    const int o = S.pack_blk_off[p];
+    for (int j = ln; j < n; j += 32)
+      if (o + j < S.cap_blk) S.pack_blk[o + j] = w.bt[(int64_t)rep * w.stride + a0 + j];
+  }
+
+  // chunk (pages, power of two): minimise the makespan estimate
+  // over the candidates whose units, member slots and items fit the capacities
+  int maxp = 1;
+  {
+    __shared__ int s_maxp;
+    if (t == 0) s_maxp = 1;
+    __syncthreads();
+    for (int p = t; p < NP; p += nt) atomicMax(&s_maxp, pk_pages(p));
+    __syncthreads();
+    maxp = s_maxp;
+  }
+  if (t == 0) s_chunk = maxp;
+  __syncthreads();
+  {
+    __shared__ float s_work, s_worst, s_bytes;
+    __shared__ int s_units, s_memb, s_items;
+    // longest-first claims over the lanes finish near max(work / lanes, longest
+    // item) plus about half a mean item of tail
+    float best = 3.0e38f;
+    int best_c = maxp;
+    for (int c = 1;; c *= 2) {
+      const int cc = min(c, maxp);
+      if (t == 0) s_work = s_worst = s_bytes = 0.f, s_units = s_memb = s_items = 0;
+      __syncthreads();
+      float work = 0.f, worst = 0.f, bytes = 0.f;
+      int units = 0, memb = 0, its = 0;
+      for (int p = t; p < NP; p += nt) {
+        const int pages = pk_pages(p), rows = pk_rows(p), kv = pk_kv(p);
+        const int parts = (pages + cc - 1) / cc;
+        const int rb = (rows + 127) / 128;
+        const int big = (pages + parts - 1) / parts;
+        const float it = sched_item_ns(S, min(rows, 128), min(big * w.bs, kv));
+        work += it * rb * parts * S.KVH;
+        worst = fmaxf(worst, it);
+        bytes += (float)kv * S.KVH * S.d * 4.f;
+        if (parts > 1) bytes += (float)parts * (rows / S.G) * S.H * S.d * 8.f;
+        units += parts;
+        memb += parts * (rows / S.G);
+        its += parts * rb * S.KVH;
+      }
+      atomicAdd(&s_work, work);
+      atomicAdd(&s_bytes, bytes);
+      atomicMax((int*)&s_worst, __float_as_int(worst));  // non-negative floats order as ints
+      atomicAdd(&s_units, units);
+      atomicAdd(&s_memb, memb);
+      atomicAdd(&s_items, its);
+      __syncthreads();
+      const float mean = s_items > 0 ? s_work / s_items : 0.f;
+      const float est = fmaxf(s_bytes / S.hbm_bpns, fmaxf(s_work / S.lanes, s_worst) + 0.5f * mean);
+      const bool fits = s_units <= S.cap_units && s_memb <= S.cap_members && s_items <= S.cap_items &&
+                        s_memb <= S.cap_slots;
+      if (fits && est <= best * 1.02f) {
+        if (est < best) best = est;
+        best_c = cc;
+      }
+      __syncthreads();
+      if (cc >= maxp) break;
+    }
+    if (t == 0) s_chunk = best_c;
+    __syncthreads();
+  }
+  const int chunk = s_chunk;
+
+  // units: pack p -> parts[p] near-equal page runs, larger first, the last
+  // carrying the partial block (simulator.py:137-154)
+  for (int p = t; p < NP; p += nt) S.parts[p] = (pk_pages(p) + chunk - 1) / chunk;
+  __syncthreads();
+  const int NU = cta_scan(NP, [&](int p) { return S.parts[p]; }, [&](int i, int v) { S.ubase[i] = v; });
+  if (t == 0) S.ubase[NP] = NU;
+  __syncthreads();
+  for (int p = wp; p < NP; p += nwp) {
+    const int parts = S.parts[p], pages = pk_pages(p), kv = pk_kv(p), u0 = S.ubase[p];
+    const int base = pages / parts, extra = pages % parts;
+    for (int i = ln; i < parts; i += 32) {
+      const int take = base + (i < extra ? 1 : 0);
+      const int pos = i * base + min(i, extra);
+      S.unit_pack[u0 + i] = p;
+      S.unit_page0[u0 + i] = pos;
+      S.unit_ntok[u0 + i] = min(take * w.bs, kv - pos * w.bs);
+    }
+  }
+  __syncthreads();
+  // member CSR of the units: unit u of pack p has the pack's members
+  const int NM = cta_scan(NU, [&](int u) { const int p = S.unit_pack[u]; return w.p_qoff[p + 1] - w.p_qoff[p]; },
+                          [&](int i, int v) { S.unit_slot_off[i] = v; });
+  if (t == 0) S.unit_slot_off[NU] = NM;
+
+  // slots: a query covered by more than one unit gets one slot per unit, in
+  // unit order (the reference fold order, attention.py:228-235)
+  for (int q = t; q < w.B; q += nt) S.qcnt[q] = 0, S.qlist_n[q] = 0;
+  __syncthreads();
+  const int D1 = w.D + 1;
+  for (int p = wp; p < NP; p += nwp)
+    for (int j = w.p_qoff[p] + ln; j < w.p_qoff[p + 1]; j += 32) {
+      const int q = w.p_q[j];
+      atomicAdd(&S.qcnt[q], S.parts[p]);
+      const int k = atomicAdd(&S.qlist_n[q], 1);
+      if (k < D1) S.qlist[(int64_t)q * D1 + k] = make_int2(p, j);
+    }
+  __syncthreads();
+  for (int q = t; q < w.B; q += nt) {  // this query's packs in pack order -> units before each
+    int2* L = S.qlist + (int64_t)q * D1;
+    const int n = min(S.qlist_n[q], D1);
+    for (int i = 1; i < n; ++i) {
+      const int2 x = L[i];
+      int k = i - 1;
+      while (k >= 0 && L[k].x > x.x) L[k + 1] = L[k], --k;
+      L[k + 1] = x;
+    }
+    int acc = 0;
+    for (int i = 0; i < n; ++i) {
+      S.prior[L[i].y] = acc;
+      acc += S.parts[L[i].x];
+    }
+  }
+  __syncthreads();
+  const int NS = cta_scan(w.B, [&](int q) { return S.qcnt[q] > 1 ? S.qcnt[q] : 0; },
+                          [&](int i, int v) { S.qoff[i] = v; });
+  (void)NS;
+  const int NMQ = cta_scan(w.B, [&](int q) { return S.qcnt[q] > 1 ? 1 : 0; }, [&](int q, int v) {
+    if (S.qcnt[q] > 1) S.merge_desc[v] = make_int4(q, S.qoff[q], S.qcnt[q], 0);
+  });
+  if (t == 0) *S.n_merge = NMQ;
+  for (int u = wp; u < NU; u += nwp) {
+    const int p = S.unit_pack[u], m0 = w.p_qoff[p], m1 = w.p_qoff[p + 1];
+    const int i = u - S.ubase[p];  // split index
+    for (int j = m0 + ln; j < m1; j += 32) {
+      const int q = w.p_q[j];
+      S.unit_slot[S.unit_slot_off[u] + (j - m0)] = S.qcnt[q] > 1 ? S.qoff[q] + S.prior[j] + i : -1;
+    }
+  }
+  __syncthreads();
+
+  // work items (unit x 128-row block x kv head), longest (estimated) first:
+  // units sorted by cost, descending (bitonic sort over the units in global memory)
+  int P2 = 1;
+  while (P2 < NU) P2 <<= 1;
+  for (int u = t; u < P2; u += nt) {
+    unsigned long long key = ~0ull;
+    if (u < NU) {
+      const int p = S.unit_pack[u];
+      const float c = sched_item_ns(S, min(pk_rows(p), 128), S.unit_ntok[u]) * ((pk_rows(p) + 127) / 128);
+      key = ((unsigned long long)(0xFFFFFFFFu - (unsigned)fminf(c, 4.0e9f)) << 32) | (unsigned)u;
+    }
+    S.ukey[u] = key;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = t; i < P2; i += nt) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long a = S.ukey[i], b = S.ukey[l];
+          if ((a > b) == up) S.ukey[i] = b, S.ukey[l] = a;
+        }
+      }
+      __syncthreads();
+    }
+  const int NI = cta_scan(NU, [&](int r) {
+    const int u = (int)(S.ukey[r] & 0xFFFFFFFFu);
+    return ((pk_rows(S.unit_pack[u]) + 127) / 128) * S.KVH;
+  }, [&](int r, int v) {
+    const int u = (int)(S.ukey[r] & 0xFFFFFFFFu), p = S.unit_pack[u], rows = pk_rows(p);
+    int k = v;
+    for (int r0 = 0; r0 < rows; r0 += 128)
+      for (int h = 0; h < S.KVH; ++h, ++k)
+        S.items[k] = Item{u, h, r0, min(128, rows - r0), S.pack_blk_off[p] + S.unit_page0[u], S.unit_ntok[u],
+                          w.p_qoff[p], S.unit_slot_off[u]};
+  });
+  if (t < NUM_VARIANTS) {
+    S.n_items[t] = t == VAR_TC ? NI : 0;
+    S.n_pair[t] = 0;
+  }
+}
+
+}  // namespace dev
+}  // namespace pat
+
+struct pat_decoder {
+  int Bmax = 0, maxb = 0, bs = 16, H = 0, KVH = 0, d = 0, D = 0, num_sms = 148, device = -1;
+  void* arena = nullptr;
+  pat::dev::Ws w{};
+  pat::dev::Sched S{};
+  pat::DevPlan plan{};
+  unsigned long long* h_new = nullptr;
+  unsigned long long* h_old = nullptr;
+  int32_t* run = nullptr;
+  int32_t* nrun = nullptr;
+  // TMA descriptors of the last (k_cache, v_cache) pair, under mu
+  std::mutex mu;
+  CUtensorMap tmk, tmv;
+  const void* tm_k = nullptr;
+  const void* tm_v = nullptr;
+  int64_t tm_blocks = -1;
+  int tm_dtype = -1;
+};
+
+extern "C" {
+
+int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t max_blocks, int32_t block_size,
+                       pat_decoder** out) {
+  using namespace pat;
+  if (!out || !opt) return PAT_ERR_INVALID_SPEC;
+  *out = nullptr;
+  if (max_batch < 1 || max_batch > 4096 || max_blocks < 1 || block_size < 16 || block_size % 16 ||
+      opt->num_heads <= 0 || opt->num_kv_heads <= 0 || opt->num_heads % opt->num_kv_heads ||
+      (opt->head_dim != 64 && opt->head_dim != 128)) {
+    set_error("pat_decoder_create: need 1 <= max_batch <= 4096, block_size a multiple of 16, head_dim 64/128, "
+              "H a multiple of KVH");
+    return PAT_ERR_INVALID_SPEC;
+  }
+  pat_decoder* Dc = new pat_decoder();
+  Dc->Bmax = max_batch;
+  Dc->maxb = max_blocks;
+  Dc->bs = block_size;
+  Dc->H = opt->num_heads;
+  Dc->KVH = opt->num_kv_heads;
+  Dc->d = opt->head_dim;
+  cudaGetDevice(&Dc->device);
+  int nsm = 0;
+  if (opt->num_sms > 0) nsm = opt->num_sms;
+  else if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, Dc->device) != cudaSuccess || nsm <= 0)
+    nsm = 148;
+  Dc->num_sms = nsm;
+  const int B = max_batch, D = std::min(B, max_blocks + 1) + 1, D1 = D + 1;
+  Dc->D = D;
+  const size_t BB = (size_t)B * B, BD = (size_t)B * D, BD1 = (size_t)B * D1, N2 = 2 * (size_t)B + 2;
+  const int G = Dc->H / Dc->KVH;
+  // capacities of the schedule (the chunk choice keeps the plan inside them)
+  const size_t cap_blk = (size_t)B * max_blocks;
+  const size_t cap_units = N2 + (size_t)B * max_blocks / 8 + 64;
+  const size_t cap_members = BD1 * 4 + 64;
+  const size_t cap_slots = (size_t)B * 16;
+  const size_t cap_items = cap_units * ((size_t)(B * G + 127) / 128) * Dc->KVH;
+  const size_t cap_items_c = std::min<size_t>(cap_items, (size_t)1 << 20);
+  size_t P2 = 1;
+  while (P2 < cap_units) P2 <<= 1;
+  struct F { void** p; size_t bytes; };
+  dev::Ws& w = Dc->w;
+  dev::Sched& S = Dc->S;
+  std::vector<F> f = {
+      {(void**)&w.nblk, B * 4}, {(void**)&w.valid, B * 4}, {(void**)&w.err, 8}, {(void**)&w.lcp, BB * 4},
+      {(void**)&w.K, B * 4}, {(void**)&w.hasleaf, B * 4}, {(void**)&w.end, BD * 4}, {(void**)&w.nq, BD * 4},
+      {(void**)&w.minq, BD * 4}, {(void**)&w.term, BD * 4}, {(void**)&w.start, BD1 * 4}, {(void**)&w.stop, BD1 * 4},
+      {(void**)&w.span, BD1 * 4}, {(void**)&w.anchor, BD1 * 4}, {(void**)&w.member, BD1 * 4},
+      {(void**)&w.nmemb, B * 4}, {(void**)&w.k0, B * 4}, {(void**)&w.cnt_own, B * 4}, {(void**)&w.pi, B * 4},
+      {(void**)&w.order, B * 4}, {(void**)&w.base, (B + 1) * 4}, {(void**)&w.n_hi, N2 * 4},
+      {(void**)&w.n_lo, N2 * 4}, {(void**)&w.n_cnt, N2 * 4}, {(void**)&w.n_depth, N2 * 4},
+      {(void**)&w.n_rep, N2 * 4}, {(void**)&w.n_a0, N2 * 4}, {(void**)&w.n_a1, N2 * 4},
+      {(void**)&w.n_span, N2 * 4}, {(void**)&w.n_pack, N2 * 4}, {(void**)&w.npacks, 4},
+      {(void**)&w.p_node, N2 * 4}, {(void**)&w.p_qoff, (N2 + 1) * 4}, {(void**)&w.p_q, BD1 * 4},
+      {(void**)&w.p_partial, N2 * 4},
+      {(void**)&S.pack_blk_off, (N2 + 1) * 4}, {(void**)&S.pack_blk, cap_blk * 4},
+      {(void**)&S.unit_pack, cap_units * 4}, {(void**)&S.unit_page0, cap_units * 4},
+      {(void**)&S.unit_ntok, cap_units * 4}, {(void**)&S.unit_slot_off, (cap_units + 1) * 4},
+      {(void**)&S.unit_slot, cap_members * 4}, {(void**)&S.items, cap_items_c * sizeof(Item)},
+      {(void**)&S.n_items, 16}, {(void**)&S.n_pair, 16}, {(void**)&S.merge_desc, B * 16},
+      {(void**)&S.n_merge, 4}, {(void**)&S.parts, N2 * 4}, {(void**)&S.ubase, (N2 + 1) * 4},
+      {(void**)&S.qcnt, B * 4}, {(void**)&S.qoff, B * 4}, {(void**)&S.qlist_n, B * 4},
+      {(void**)&S.qlist, BD1 * 8}, {(void**)&S.prior, BD1 * 4}, {(void**)&S.ukey, P2 * 8},
+      {(void**)&Dc->h_new, 8}, {(void**)&Dc->h_old, 8}, {(void**)&Dc->run, 4}, {(void**)&Dc->nrun, 4}};
+  size_t total = 0;
+  for (auto& x : f) total += (x.bytes + 255) & ~size_t(255);
+  if (cudaMalloc(&Dc->arena, total) != cudaSuccess) {
+    set_error("pat_decoder_create: %zu bytes of device state", total);
+    delete Dc;
+    return PAT_ERR_CUDA;
+  }
+  cudaMemset(Dc->arena, 0, total);
+  size_t off = 0;
+  for (auto& x : f) {
+    *x.p = (uint8_t*)Dc->arena + off;
+    off += (x.bytes + 255) & ~size_t(255);
+  }
+  cudaMemset(Dc->h_old, 0xFF, 8);  // never equal to a real fingerprint's first value
+  w.D = D;
+  w.bs = block_size;
+  w.run = Dc->run;
+  S.cap_blk = (int)cap_blk;
+  S.cap_units = (int)cap_units;
+  S.cap_members = (int)cap_members;
+  S.cap_items = (int)cap_items_c;
+  S.cap_slots = (int)cap_slots;
+  const pat_cost_model cm = cost_model();
+  S.item_ns = (float)cm.tc_item_ns;
+  S.row_ns = (float)cm.tc_item_row_ns;
+  S.step_ns = (float)cm.tc_step_ns;
+  S.hbm_bpns = (float)cm.hbm_bytes_per_ns;
+  S.lanes = 2 * Dc->num_sms;
+  S.H = Dc->H;
+  S.KVH = Dc->KVH;
+  S.d = Dc->d;
+  S.G = G;
+  DevPlan& P = Dc->plan;
+  P.pack_q_off = w.p_qoff;
+  P.pack_q = w.p_q;
+  P.pack_blk_off = S.pack_blk_off;
+  P.pack_blk = S.pack_blk;
+  P.unit_pack = S.unit_pack;
+  P.unit_page0 = S.unit_page0;
+  P.unit_ntok = S.unit_ntok;
+  P.unit_slot_off = S.unit_slot_off;
+  P.unit_slot = S.unit_slot;
+  for (int v = 0; v < NUM_VARIANTS; ++v) P.items[v] = S.items;
+  P.n_items = S.n_items;
+  P.n_pair = S.n_pair;
+  P.merge_desc = S.merge_desc;
+  P.n_merge = S.n_merge;
+  P.H = Dc->H;
+  P.KVH = Dc->KVH;
+  P.d = Dc->d;
+  P.G = G;
+  P.bs = block_size;
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_error("pat_decoder_create: device initialisation failed");
+    cudaFree(Dc->arena);
+    delete Dc;
+    return PAT_ERR_CUDA;
+  }
+  *out = Dc;
+  return PAT_OK;
+}
+
+size_t pat_decoder_workspace_bytes(const pat_decoder* Dc) {
+  if (!Dc) return 0;
+  const size_t so = (size_t)Dc->S.cap_slots * Dc->H * Dc->d * 4, sl = (size_t)Dc->S.cap_slots * Dc->H * 4;
+  return ((so + 255) & ~size_t(255)) + ((sl + 255) & ~size_t(255)) + 256;
+}
+
+int pat_decoder_forward(pat_decoder* Dc, const int32_t* block_tables, int64_t bt_stride, const int32_t* seq_lens,
+                        int32_t B, int32_t max_blocks, const void* q, const void* k_cache, const void* v_cache,
+                        int64_t num_pool_blocks, void* out, void* workspace, size_t workspace_bytes, int32_t dtype,
+                        float scale, int32_t flags, void* stream) {
+  using namespace pat;
+  if (!Dc) return PAT_ERR_INVALID_SPEC;
+  if (B < 0 || B > Dc->Bmax || max_blocks < 1 || max_blocks > Dc->maxb || bt_stride < max_blocks ||
+      (B > 0 && (!block_tables || !seq_lens || !q || !k_cache || !v_cache || !out))) {
+    set_error("pat_decoder_forward: table of %d x %d exceeds the decoder's %d x %d (or null pointers)", B, max_blocks,
+              Dc->Bmax, Dc->maxb);
+    return PAT_ERR_SHAPE_MISMATCH;
+  }
+  if (dtype != PAT_DTYPE_F16 && dtype != PAT_DTYPE_BF16) {
+    set_error("dtype must be f16 or bf16");
+    return PAT_ERR_NO_FEASIBLE_CONFIG;
+  }
+  if (workspace_bytes < pat_decoder_workspace_bytes(Dc)) {
+    set_error("workspace %zu < required %zu", workspace_bytes, pat_decoder_workspace_bytes(Dc));
+    return PAT_ERR_WORKSPACE;
+  }
+  if (B == 0) return PAT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUtensorMap tmk, tmv;
+  {
+    std::lock_guard<std::mutex> lk(Dc->mu);
+    if (Dc->tm_k != k_cache || Dc->tm_v != v_cache || Dc->tm_blocks != num_pool_blocks || Dc->tm_dtype != dtype) {
+      const int e1 = make_kv_tensor_map(&Dc->tmk, k_cache, num_pool_blocks, Dc->bs, Dc->KVH, Dc->d, dtype);
+      const int e2 = make_kv_tensor_map(&Dc->tmv, v_cache, num_pool_blocks, Dc->bs, Dc->KVH, Dc->d, dtype);
+      if (e1 || e2) {
+        Dc->tm_k = nullptr;
+        set_error("cuTensorMapEncodeTiled failed (%d, %d)", e1, e2);
+        return PAT_ERR_CUDA;
+      }
+      Dc->tm_k = k_cache;
+      Dc->tm_v = v_cache;
+      Dc->tm_blocks = num_pool_blocks;
+      Dc->tm_dtype = dtype;
+    }
+    tmk = Dc->tmk;
+    tmv = Dc->tmv;
+  }
+  dev::Ws w = Dc->w;
+  w.bt = block_tables;
+  w.stride = bt_stride;
+  w.seq = seq_lens;
+  w.B = B;
+  w.maxb = max_blocks;
+  dev::Sched S = Dc->S;
+  S.w = w;
+  const int N2 = 2 * B + 2;
+  if (!(flags & PAT_DECODE_SAME_TABLE)) {
+  // 1. fingerprint of (block_tables, seq_lens); re-plan only when it changed
+  dev::k_hash_seed<<<1, 1, 0, st>>>(Dc->h_new, B, Dc->bs);
+  k_table_hash<<<std::min(148 * 4, (B + 7) / 8), 256, 0, st>>>(block_tables, bt_stride, seq_lens, B, Dc->bs,
+                                                               Dc->h_new);
+  dev::k_hash_check<<<1, 1, 0, st>>>(Dc->h_new, Dc->h_old, Dc->run, Dc->nrun);
+  // 2. GPU packer (every kernel returns at once when the table is unchanged)
+  const int TB = 128, gq = (B + TB - 1) / TB;
+  dev::k_reset<<<64, 256, 0, st>>>(w, N2);
+  dev::k_rows<<<gq, TB, 0, st>>>(w);
+  int P = 1;
+  while (P < std::max(B, max_blocks)) P <<= 1;
+  const int dup_smem = P * 4;
+  if (dup_smem > 48 * 1024) cudaFuncSetAttribute(dev::k_dup, cudaFuncAttributeMaxDynamicSharedMemorySize, dup_smem);
+  dev::k_dup<<<B, 256, dup_smem, st>>>(w);
+  dev::k_lcp<<<(int)std::min<int64_t>(((int64_t)B * B * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(w);
+  int PB = 1;
+  while (PB < B) PB <<= 1;
+  if (PB * 8 > 48 * 1024) cudaFuncSetAttribute(dev::k_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, PB * 8);
+  dev::k_levels<<<B, 256, PB * 8, st>>>(w);
+  dev::k_decide<<<gq, TB, 0, st>>>(w);
+  dev::k_rank<<<(B * 32 + 255) / 256, 256, 0, st>>>(w);
+  dev::k_scan_nodes<<<1, 1024, 0, st>>>(w);
+  dev::k_nodes_init<<<64, 256, 0, st>>>(w);
+  dev::k_nodes<<<gq, TB, 0, st>>>(w);
+  dev::k_order<<<64, 256, 0, st>>>(w);
+  dev::k_pack_offsets<<<1, 1, 0, st>>>(w);
+  dev::k_members<<<gq, TB, 0, st>>>(w);
+  // 3. schedule on the device
+  dev::k_schedule<<<1, 1024, 0, st>>>(S);
+  }
+  // 4. forward + merge over the device plan (counts read on the device)
+  float* po = (float*)workspace;
+  const size_t so = ((size_t)Dc->S.cap_slots * Dc->H * Dc->d * 4 + 255) & ~size_t(255);
+  float* pl = (float*)((uint8_t*)workspace + so);
+  int32_t* sched = (int32_t*)((uint8_t*)workspace + pat_decoder_workspace_bytes(Dc) - 256);
+  if (cudaMemsetAsync(sched, 0, 16, st) != cudaSuccess) {
+    set_error("pat_decoder_forward: counter reset failed");
+    return PAT_ERR_CUDA;
+  }
+  if (scale <= 0.f) scale = 1.0f / sqrtf((float)Dc->d);
+  const float scale_log2 = scale * 1.4426950408889634f;
+  cudaError_t e = launch_forward_tc(tmk, tmv, Dc->plan, VAR_TC, Dc->num_sms, dtype, Dc->d, q, out, po, pl, scale_log2,
+                                    sched, st);
+  if (e == cudaSuccess) e = launch_merge(Dc->plan, Dc->num_sms * 8, dtype, Dc->d, po, pl, out, st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("pat_decoder_forward: %s", cudaGetErrorString(e));
+    return PAT_ERR_CUDA;
+  }
+  return PAT_OK;
+}
+
+int pat_decoder_status(pat_decoder* Dc, void* stream, int32_t* replans) {
+  if (!Dc) return PAT_ERR_INVALID_SPEC;
+  int32_t err[2] = {0, 0}, n = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyAsync(err, Dc->w.err, 8, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&n, Dc->nrun, 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) {
+    pat::set_error("pat_decoder_status: %s", cudaGetErrorString(cudaGetLastError()));
+    return PAT_ERR_CUDA;
+  }
+  if (replans) *replans = n;
+  if (err[0] == PAT_ERR_INVALID_SPEC) pat::set_error("row %d: empty, too long, or repeats a block ID", err[1]);
+  else if (err[0]) pat::set_error("query %d: prefix forest deeper than the device packer capacity", err[1]);
+  return err[0];
+}
+
+void pat_decoder_destroy(pat_decoder* Dc) {
+  if (!Dc) return;
+  if (Dc->arena) cudaFree(Dc->arena);
+  delete Dc;
+}
+
+}  // extern "C"
+
+// Debug / test export of the device plan (synchronising copy of one array).
+//  what: 0 npacks[1] 1 p_qoff 2 p_q 3 pack_blk_off 4 pack_blk 5 unit_pack 6 unit_page0
+//        7 unit_ntok 8 unit_slot_off 9 unit_slot 10 items (8 ints each) 11 n_items[4]
+//        12 merge_desc (4 ints each) 13 n_merge[1] 14 p_node 15 parts
+extern "C" int pat_decoder_debug_export(pat_decoder* Dc, int32_t what, int32_t* host, int64_t n_ints) {
+  if (!Dc || !host) return PAT_ERR_INVALID_SPEC;
+  const void* src = nullptr;
+  switch (what) {
+    case 0: src = Dc->w.npacks; break;
+    case 1: src = Dc->w.p_qoff; break;
+    case 2: src = Dc->w.p_q; break;
+    case 3: src = Dc->S.pack_blk_off; break;
+    case 4: src = Dc->S.pack_blk; break;
+    case 5: src = Dc->S.unit_pack; break;
+    case 6: src = Dc->S.unit_page0; break;
+    case 7: src = Dc->S.unit_ntok; break;
+    case 8: src = Dc->S.unit_slot_off; break;
+    case 9: src = Dc->S.unit_slot; break;
+    case 10: src = Dc->S.items; break;
+    case 11: src = Dc->S.n_items; break;
+    case 12: src = Dc->S.merge_desc; break;
+    case 13: src = Dc->S.n_merge; break;
+    case 14: src = Dc->w.p_node; break;
+    case 15: src = Dc->S.parts; break;
+    default: return PAT_ERR_INVALID_SPEC;
+  }
+  return cudaMemcpy(host, src, (size_t)n_ints * 4, cudaMemcpyDeviceToHost) == cudaSuccess ? PAT_OK : PAT_ERR_CUDA;
 }

@@ -33,17 +33,18 @@ from vllm.v1.attention.backend import AttentionCGSupport
 
 
 class PatAttentionMetadataBuilder(FlashAttentionMetadataBuilder):
-    """FlashAttention's metadata with full-CUDA-graph capture of attention turned
-    off: the PAT op looks its plan up by a device fingerprint of the block table
-    that the host reads back, and packs a new plan on a miss -- host work a
-    captured graph would freeze (vLLM then runs attention eagerly between its
-    piecewise graphs)."""
+    """FlashAttention's metadata; full CUDA graphs of decode-only batches
+    (``max_query_len == 1``, the batches PAT serves).  The PAT op plans on the
+    GPU (``pat_decoder``: device fingerprint, packer and scheduler, no host
+    synchronisation), so a captured decode graph re-plans on the device when
+    vLLM rewrites its block table in place.  Mixed / prefill batches stay with
+    FlashAttention (piecewise graphs)."""
 
-    _cudagraph_support = AttentionCGSupport.NEVER
+    _cudagraph_support = AttentionCGSupport.UNIFORM_SINGLE_TOKEN_DECODE
 
     @classmethod
     def get_cudagraph_support(cls, vllm_config, kv_cache_spec) -> AttentionCGSupport:
-        return AttentionCGSupport.NEVER
+        return AttentionCGSupport.UNIFORM_SINGLE_TOKEN_DECODE
 
 
 class PatAttentionImpl(FlashAttentionImpl):
