@@ -79,26 +79,33 @@ struct Ws {
 __device__ __forceinline__ int tok_at(const Ws& w, int q, int p) { return p == w.nblk[q] - 1 ? w.valid[q] : w.bs; }
 __device__ __forceinline__ int blk_at(const Ws& w, int q, int p) { return w.bt[(int64_t)q * w.stride + p]; }
 
+// Each phase is a __device__ function written for any grid (grid-stride /
+// block-stride loops, block-uniform control flow), launched either as its own
+// kernel (pat_plan_create_device) or inside the persistent planner kernel of
+// the device decoder, separated by grid barriers.
+#define PAT_GRID_LOOP(i, n) for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += gridDim.x * blockDim.x)
+
+__device__ void ph_rows(const Ws& w) {
+  PAT_GRID_LOOP(q, w.B) {
+    int s = w.seq[q];
+    int n = s > 0 ? (s + w.bs - 1) / w.bs : 0;
+    w.nblk[q] = n;
+    w.valid[q] = s - (n - 1) * w.bs;
+    if (n <= 0 || n > w.maxb) {
+      if (atomicCAS(&w.err[0], 0, PAT_ERR_INVALID_SPEC) == 0) w.err[1] = q;
+    }
+  }
+}
 __global__ void k_rows(Ws w) {
   if (w.run && !*w.run) return;
-  int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= w.B) return;
-  int s = w.seq[q];
-  int n = s > 0 ? (s + w.bs - 1) / w.bs : 0;
-  w.nblk[q] = n;
-  w.valid[q] = s - (n - 1) * w.bs;
-  if (n <= 0 || n > w.maxb) {
-    if (atomicCAS(&w.err[0], 0, PAT_ERR_INVALID_SPEC) == 0) w.err[1] = q;
-  }
+  ph_rows(w);
 }
 
 // one CTA per row: bitonic sort of the row's block ids in smem, adjacent compare
-__global__ void k_dup(Ws w) {
-  if (w.run && !*w.run) return;
-  extern __shared__ int32_t sbuf[];
-  const int q = blockIdx.x;
+__device__ void ph_dup(const Ws& w, int32_t* sbuf) {
+  for (int q = blockIdx.x; q < w.B; q += gridDim.x) {
   const int n = min(w.nblk[q], w.maxb);
-  if (n <= 1) return;
+  if (n <= 1) continue;
   int P = 1;
   while (P < n) P <<= 1;
   for (int i = threadIdx.x; i < P; i += blockDim.x) sbuf[i] = i < n ? blk_at(w, q, i) : 0x7fffffff;
@@ -122,11 +129,17 @@ __global__ void k_dup(Ws w) {
     if (sbuf[i] == sbuf[i + 1]) {
       if (atomicCAS(&w.err[0], 0, PAT_ERR_INVALID_SPEC) == 0) w.err[1] = q;
     }
+  __syncthreads();
+  }
+}
+__global__ void k_dup(Ws w) {
+  if (w.run && !*w.run) return;
+  extern __shared__ int32_t sbuf[];
+  ph_dup(w, sbuf);
 }
 
 // one warp per (q, r) pair with q < r
-__global__ void k_lcp(Ws w) {
-  if (w.run && !*w.run) return;
+__device__ void ph_lcp(const Ws& w) {
   const int lane = threadIdx.x & 31;
   const int64_t npairs = (int64_t)w.B * w.B;
   for (int64_t pr = (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) / 32; pr < npairs;
@@ -152,12 +165,14 @@ __global__ void k_lcp(Ws w) {
     if (lane == 0) w.lcp[(int64_t)q * w.B + r] = w.lcp[(int64_t)r * w.B + q] = l;
   }
 }
+__global__ void k_lcp(Ws w) {
+  if (w.run && !*w.run) return;
+  ph_lcp(w);
+}
 
 // one CTA per query: sort (lcp, r) keys, derive the internal levels
-__global__ void k_levels(Ws w) {
-  if (w.run && !*w.run) return;
-  extern __shared__ unsigned long long skey[];
-  const int q = blockIdx.x;
+__device__ void ph_levels(const Ws& w, unsigned long long* skey) {
+  for (int q = blockIdx.x; q < w.B; q += gridDim.x) {
   int P = 1;
   while (P < w.B) P <<= 1;
   const int32_t* L = w.lcp + (int64_t)q * w.B;
@@ -202,7 +217,8 @@ __global__ void k_levels(Ws w) {
       }
       if (Kq >= w.D) {
         if (atomicCAS(&w.err[0], 0, PAT_ERR_NO_FEASIBLE_CONFIG) == 0) w.err[1] = q;
-        return;
+        M = -1;  // abandon this query (the plan is rejected)
+        break;
       }
       w.end[(int64_t)q * w.D + Kq] = v;
       w.nq[(int64_t)q * w.D + Kq] = 1 + (M - i);
@@ -212,6 +228,7 @@ __global__ void k_levels(Ws w) {
       i = j;
     }
     // resolve minimum member of {r : lcp >= end_k} u {q} via a backward suffix min
+    if (M < 0) Kq = 0, M = 0;
     int k = Kq - 1;
     for (int e = M - 1; e >= 0 && k >= 0; --e) {
       sufmin = min(sufmin, (int)(skey[e] & 0xffffffffu));
@@ -223,6 +240,13 @@ __global__ void k_levels(Ws w) {
     w.K[q] = Kq;
     w.hasleaf[q] = (Kq == 0) || w.end[(int64_t)q * w.D + Kq - 1] < nbq;
   }
+  __syncthreads();
+  }
+}
+__global__ void k_levels(Ws w) {
+  if (w.run && !*w.run) return;
+  extern __shared__ unsigned long long skey[];
+  ph_levels(w, skey);
 }
 
 __device__ __forceinline__ int levels_of(const Ws& w, int q) { return w.K[q] + (w.hasleaf[q] ? 1 : 0); }
@@ -237,10 +261,8 @@ __device__ __forceinline__ int64_t span_tokens(const Ws& w, int q, int a, int b)
 }
 
 // thread per query: TreeHeuristic decisions along the path + ownership
-__global__ void k_decide(Ws w) {
-  if (w.run && !*w.run) return;
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= w.B) return;
+__device__ void ph_decide(const Ws& w) {
+  PAT_GRID_LOOP(q, w.B) {
   const int K = w.K[q], Lv = levels_of(w, q), D1 = w.D + 1;
   int span = 0, anchor = 0, nm = 0;
   for (int k = 0; k < Lv; ++k) {
@@ -271,6 +293,11 @@ __global__ void k_decide(Ws w) {
   while (k0 < Lv && owner_of(w, q, k0) != q) ++k0;
   w.k0[q] = k0;
   w.cnt_own[q] = Lv - k0;
+  }
+}
+__global__ void k_decide(Ws w) {
+  if (w.run && !*w.run) return;
+  ph_decide(w);
 }
 
 // lexicographic key element e of query q: e=0 root group min, e=1+k slot at level k
@@ -283,10 +310,9 @@ __device__ __forceinline__ int key_at(const Ws& w, int q, int e) {
 }
 
 // warp per query: pi(q) = #{r : key(r) < key(q)}
-__global__ void k_rank(Ws w) {
-  if (w.run && !*w.run) return;
-  const int q = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
-  if (q >= w.B) return;
+__device__ void ph_rank(const Ws& w) {
+  const int lane = threadIdx.x & 31;
+  for (int q = (blockIdx.x * blockDim.x + threadIdx.x) / 32; q < w.B; q += gridDim.x * blockDim.x / 32) {
   const int lq = w.K[q] + 1;
   int cnt = 0;
   for (int r = lane; r < w.B; r += 32) {
@@ -312,11 +338,16 @@ __global__ void k_rank(Ws w) {
     w.pi[q] = cnt;
     w.order[cnt] = q;
   }
+  }
+}
+__global__ void k_rank(Ws w) {
+  if (w.run && !*w.run) return;
+  ph_rank(w);
 }
 
 // single CTA exclusive scan of cnt_own -> base
-__global__ void k_scan_nodes(Ws w) {
-  if (w.run && !*w.run) return;
+__device__ void ph_scan_nodes(const Ws& w) {
+  if (blockIdx.x != 0) return;  // one CTA of up to 1024 threads
   __shared__ int32_t part[1024];
   const int t = threadIdx.x, n = w.B;
   const int per = (n + blockDim.x - 1) / blockDim.x;
@@ -340,14 +371,17 @@ __global__ void k_scan_nodes(Ws w) {
     acc += w.cnt_own[i];
   }
 }
+__global__ void k_scan_nodes(Ws w) {
+  if (w.run && !*w.run) return;
+  ph_scan_nodes(w);
+}
 
 __device__ __forceinline__ int node_id(const Ws& w, int q, int k) {
   const int m = owner_of(w, q, k);
   return w.base[m] + k - w.k0[m];
 }
 
-__global__ void k_nodes_init(Ws w) {
-  if (w.run && !*w.run) return;
+__device__ void ph_nodes_init(const Ws& w) {
   const int N = w.base[w.B];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     w.n_hi[i] = 0;
@@ -356,12 +390,14 @@ __global__ void k_nodes_init(Ws w) {
     w.n_pack[i] = -1;
   }
 }
+__global__ void k_nodes_init(Ws w) {
+  if (w.run && !*w.run) return;
+  ph_nodes_init(w);
+}
 
 // thread per query: every level it passes through
-__global__ void k_nodes(Ws w) {
-  if (w.run && !*w.run) return;
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= w.B) return;
+__device__ void ph_nodes(const Ws& w) {
+  PAT_GRID_LOOP(q, w.B) {
   const int Lv = levels_of(w, q), D1 = w.D + 1;
   const int pq = w.pi[q];
   for (int k = 0; k < Lv; ++k) {
@@ -377,11 +413,15 @@ __global__ void k_nodes(Ws w) {
       w.n_span[id] = w.span[(int64_t)q * D1 + k];
     }
   }
+  }
+}
+__global__ void k_nodes(Ws w) {
+  if (w.run && !*w.run) return;
+  ph_nodes(w);
 }
 
 // thread per node: rank among emitting nodes by (hi asc, depth desc)
-__global__ void k_order(Ws w) {
-  if (w.run && !*w.run) return;
+__device__ void ph_order(const Ws& w) {
   const int N = w.base[w.B];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     if (w.n_cnt[i] == 0) continue;
@@ -397,10 +437,14 @@ __global__ void k_order(Ws w) {
     atomicAdd(w.npacks, 1);
   }
 }
+__global__ void k_order(Ws w) {
+  if (w.run && !*w.run) return;
+  ph_order(w);
+}
 
 // single thread: query offsets per pack (packs <= 2B)
-__global__ void k_pack_offsets(Ws w) {
-  if (w.run && !*w.run) return;
+__device__ void ph_pack_offsets(const Ws& w) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
   const int np = *w.npacks;
   int acc = 0;
   for (int p = 0; p < np; ++p) {
@@ -410,12 +454,14 @@ __global__ void k_pack_offsets(Ws w) {
   }
   w.p_qoff[np] = acc;
 }
+__global__ void k_pack_offsets(Ws w) {
+  if (w.run && !*w.run) return;
+  ph_pack_offsets(w);
+}
 
 // thread per query: place it in each pack it belongs to, in pi order
-__global__ void k_members(Ws w) {
-  if (w.run && !*w.run) return;
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= w.B) return;
+__device__ void ph_members(const Ws& w) {
+  PAT_GRID_LOOP(q, w.B) {
   const int Lv = levels_of(w, q), D1 = w.D + 1;
   const int pq = w.pi[q];
   for (int k = 0; k < Lv; ++k) {
@@ -431,6 +477,11 @@ __global__ void k_members(Ws w) {
     w.p_q[w.p_qoff[p] + pos] = q;
     if (w.nmemb[q] > 1) atomicOr(&w.p_partial[p], 1);
   }
+  }
+}
+__global__ void k_members(Ws w) {
+  if (w.run && !*w.run) return;
+  ph_members(w);
 }
 
 }  // namespace dev
@@ -740,9 +791,9 @@ __device__ __forceinline__ float sched_item_ns(const Sched& S, int rows, int nto
 
 // One CTA: split (chunk chosen by a makespan estimate over the lanes), units,
 // partial slots in unit order, longest-first work items, merge descriptors.
-__global__ void __launch_bounds__(1024) k_schedule(Sched S) {
+__device__ void ph_schedule(const Sched& S) {
+  if (blockIdx.x != 0) return;  // one CTA of 1024 threads
   const Ws& w = S.w;
-  if (w.run && !*w.run) return;
   const int t = threadIdx.x, nt = blockDim.x;
   __shared__ int s_np, s_err, s_chunk;
   __shared__ float s_best[32];
@@ -948,6 +999,111 @@ __global__ void __launch_bounds__(1024) k_schedule(Sched S) {
     S.n_pair[t] = 0;
   }
 }
+__global__ void __launch_bounds__(1024) k_schedule(Sched S) {
+  if (S.w.run && !*S.w.run) return;
+  ph_schedule(S);
+}
+
+// grid barrier of the persistent planner (every CTA resident: cooperative
+// launch).  The gpu-scope fence after the wait also invalidates the SM's L1,
+// so the next phase reads what other SMs wrote.
+__device__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// fingerprint terms of (block_tables, seq_lens), summed (order-free); a warp per row
+__device__ void ph_hash(const int32_t* __restrict__ bt, int64_t stride, const int32_t* __restrict__ seq, int B,
+                        int bs, unsigned long long* acc_out) {
+  const int lane = threadIdx.x & 31;
+  const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  uint64_t acc = 0;
+  for (int q = wi; q < B; q += nw) {
+    const int len = seq[q];
+    const int nb = len > 0 ? (len + bs - 1) / bs : 0;
+    const uint64_t rowk = mix64(((uint64_t)q << 32) ^ 0xA5A5A5A5ull);
+    for (int j = lane; j < nb; j += 32) acc += mix64(rowk ^ ((uint64_t)j << 32) ^ (uint32_t)bt[(int64_t)q * stride + j]);
+    if (lane == 0) acc += mix64(rowk + 0x5151ull + (uint64_t)(uint32_t)len);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0 && acc) atomicAdd(acc_out, (unsigned long long)acc);
+}
+
+struct PlanState {
+  unsigned long long* h_acc;  // fingerprint accumulator (left at 0 between calls)
+  unsigned long long* h_old;  // fingerprint of the planned table
+  int32_t* run;
+  int32_t* nrun;
+  unsigned* bar;  // [2] grid barrier
+};
+
+// The whole planner in ONE launch: fingerprint -> compare -> (only when the
+// table changed) reset, rows, duplicates, pairwise prefixes, levels, decisions,
+// DFS rank, nodes, pack order and members, then the schedule on CTA 0.
+__global__ void __launch_bounds__(1024, 1) k_plan(Ws w, Sched S, PlanState ps, int N2) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  ph_hash(w.bt, w.stride, w.seq, w.B, w.bs, ps.h_acc);
+  grid_sync(ps.bar);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long h = *ps.h_acc +
+        (((unsigned long long)(unsigned)w.B << 32) ^ (unsigned long long)(unsigned)w.bs ^ 0x7A7A000000000000ull);
+    *ps.h_acc = 0;
+    const bool changed = h != *ps.h_old;
+    *ps.run = changed ? 1 : 0;
+    if (changed) {
+      *ps.h_old = h;
+      atomicAdd(ps.nrun, 1);
+    }
+  }
+  grid_sync(ps.bar);
+  if (!*(volatile int32_t*)ps.run) return;
+  {
+    const int BD1 = w.B * (w.D + 1);
+    PAT_GRID_LOOP(i, BD1) w.member[i] = 0;
+    PAT_GRID_LOOP(i, N2) w.n_rep[i] = w.n_a0[i] = w.n_a1[i] = w.n_span[i] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) w.err[0] = w.err[1] = *w.npacks = 0;
+  }
+  grid_sync(ps.bar);
+  ph_rows(w);
+  grid_sync(ps.bar);
+  ph_dup(w, (int32_t*)dsm);
+  grid_sync(ps.bar);
+  ph_lcp(w);
+  grid_sync(ps.bar);
+  ph_levels(w, (unsigned long long*)dsm);
+  grid_sync(ps.bar);
+  ph_decide(w);
+  grid_sync(ps.bar);
+  ph_rank(w);
+  grid_sync(ps.bar);
+  ph_scan_nodes(w);
+  grid_sync(ps.bar);
+  ph_nodes_init(w);
+  grid_sync(ps.bar);
+  ph_nodes(w);
+  grid_sync(ps.bar);
+  ph_order(w);
+  grid_sync(ps.bar);
+  ph_pack_offsets(w);
+  grid_sync(ps.bar);
+  ph_members(w);
+  grid_sync(ps.bar);
+  ph_schedule(S);
+}
 
 }  // namespace dev
 }  // namespace pat
@@ -958,10 +1114,12 @@ struct pat_decoder {
   pat::dev::Ws w{};
   pat::dev::Sched S{};
   pat::DevPlan plan{};
-  unsigned long long* h_new = nullptr;
+  unsigned long long* h_new = nullptr;  // fingerprint accumulator of the planner kernel
   unsigned long long* h_old = nullptr;
   int32_t* run = nullptr;
   int32_t* nrun = nullptr;
+  unsigned* bar = nullptr;  // grid barrier of the planner kernel
+  int plan_grid = 0;
   // TMA descriptors of the last (k_cache, v_cache) pair, under mu
   std::mutex mu;
   CUtensorMap tmk, tmv;
@@ -1034,7 +1192,8 @@ int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t m
       {(void**)&S.n_merge, 4}, {(void**)&S.parts, N2 * 4}, {(void**)&S.ubase, (N2 + 1) * 4},
       {(void**)&S.qcnt, B * 4}, {(void**)&S.qoff, B * 4}, {(void**)&S.qlist_n, B * 4},
       {(void**)&S.qlist, BD1 * 8}, {(void**)&S.prior, BD1 * 4}, {(void**)&S.ukey, P2 * 8},
-      {(void**)&Dc->h_new, 8}, {(void**)&Dc->h_old, 8}, {(void**)&Dc->run, 4}, {(void**)&Dc->nrun, 4}};
+      {(void**)&Dc->h_new, 8}, {(void**)&Dc->h_old, 8}, {(void**)&Dc->run, 4}, {(void**)&Dc->nrun, 4},
+      {(void**)&Dc->bar, 8}};
   size_t total = 0;
   for (auto& x : f) total += (x.bytes + 255) & ~size_t(255);
   if (cudaMalloc(&Dc->arena, total) != cudaSuccess) {
@@ -1049,6 +1208,24 @@ int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t m
     off += (x.bytes + 255) & ~size_t(255);
   }
   cudaMemset(Dc->h_old, 0xFF, 8);  // never equal to a real fingerprint's first value
+  // the planner kernel runs one CTA per SM (all resident: cooperative launch)
+  {
+    int P = 1;
+    while (P < std::max(B, max_blocks)) P <<= 1;
+    int PB = 1;
+    while (PB < B) PB <<= 1;
+    const int dyn = std::max(P * 4, PB * 8);
+    cudaFuncSetAttribute(dev::k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_plan, 1024, dyn);
+    Dc->plan_grid = std::max(1, std::min(per_sm, 1)) * nsm;
+    if (per_sm < 1) {
+      set_error("pat_decoder_create: the planner kernel does not fit an SM");
+      cudaFree(Dc->arena);
+      delete Dc;
+      return PAT_ERR_CUDA;
+    }
+  }
   w.D = D;
   w.bs = block_size;
   w.run = Dc->run;
@@ -1154,35 +1331,22 @@ int pat_decoder_forward(pat_decoder* Dc, const int32_t* block_tables, int64_t bt
   S.w = w;
   const int N2 = 2 * B + 2;
   if (!(flags & PAT_DECODE_SAME_TABLE)) {
-  // 1. fingerprint of (block_tables, seq_lens); re-plan only when it changed
-  dev::k_hash_seed<<<1, 1, 0, st>>>(Dc->h_new, B, Dc->bs);
-  k_table_hash<<<std::min(148 * 4, (B + 7) / 8), 256, 0, st>>>(block_tables, bt_stride, seq_lens, B, Dc->bs,
-                                                               Dc->h_new);
-  dev::k_hash_check<<<1, 1, 0, st>>>(Dc->h_new, Dc->h_old, Dc->run, Dc->nrun);
-  // 2. GPU packer (every kernel returns at once when the table is unchanged)
-  const int TB = 128, gq = (B + TB - 1) / TB;
-  dev::k_reset<<<64, 256, 0, st>>>(w, N2);
-  dev::k_rows<<<gq, TB, 0, st>>>(w);
-  int P = 1;
-  while (P < std::max(B, max_blocks)) P <<= 1;
-  const int dup_smem = P * 4;
-  if (dup_smem > 48 * 1024) cudaFuncSetAttribute(dev::k_dup, cudaFuncAttributeMaxDynamicSharedMemorySize, dup_smem);
-  dev::k_dup<<<B, 256, dup_smem, st>>>(w);
-  dev::k_lcp<<<(int)std::min<int64_t>(((int64_t)B * B * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(w);
-  int PB = 1;
-  while (PB < B) PB <<= 1;
-  if (PB * 8 > 48 * 1024) cudaFuncSetAttribute(dev::k_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, PB * 8);
-  dev::k_levels<<<B, 256, PB * 8, st>>>(w);
-  dev::k_decide<<<gq, TB, 0, st>>>(w);
-  dev::k_rank<<<(B * 32 + 255) / 256, 256, 0, st>>>(w);
-  dev::k_scan_nodes<<<1, 1024, 0, st>>>(w);
-  dev::k_nodes_init<<<64, 256, 0, st>>>(w);
-  dev::k_nodes<<<gq, TB, 0, st>>>(w);
-  dev::k_order<<<64, 256, 0, st>>>(w);
-  dev::k_pack_offsets<<<1, 1, 0, st>>>(w);
-  dev::k_members<<<gq, TB, 0, st>>>(w);
-  // 3. schedule on the device
-  dev::k_schedule<<<1, 1024, 0, st>>>(S);
+    // fingerprint, compare, and (only when the table changed) GPU packer +
+    // device schedule: ONE cooperative launch (grid barriers between phases)
+    int P = 1;
+    while (P < std::max(B, max_blocks)) P <<= 1;
+    int PB = 1;
+    while (PB < B) PB <<= 1;
+    const int dyn = std::max(P * 4, PB * 8);
+    dev::PlanState ps{Dc->h_new, Dc->h_old, Dc->run, Dc->nrun, Dc->bar};
+    int n2 = N2;
+    void* args[] = {(void*)&w, (void*)&S, (void*)&ps, (void*)&n2};
+    cudaError_t le = cudaLaunchCooperativeKernel((const void*)dev::k_plan, dim3(Dc->plan_grid), dim3(1024), args,
+                                                 (size_t)dyn, st);
+    if (le != cudaSuccess) {
+      set_error("pat_decoder_forward: planner launch: %s", cudaGetErrorString(le));
+      return PAT_ERR_CUDA;
+    }
   }
   // 4. forward + merge over the device plan (counts read on the device)
   float* po = (float*)workspace;

@@ -13,7 +13,7 @@ import os
 import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PAT_KERNELS = ("fwd_tc2_kernel", "fwd_stream_kernel", "merge_kernel")
+PAT_KERNELS = ("fwd_tc4_kernel", "fwd_stream_kernel", "merge_kernel")
 
 
 def parse(path):
