@@ -325,12 +325,16 @@ def _launches(plan):
 
 def measure_e2e(P, plan, w, table, q, kc, vc, ws, steps, warmup, dev, flush):
     """End to end through the serving operator ``torch.ops.patb200.decode_attention``
-    (what the vLLM backend calls) with HOST buffers: per step one H2D copy of the
-    step's Q + block table + seq lens (one pinned staging buffer) into the tensors
-    the op reads, the op (device fingerprint of the uploaded table -- an 8-byte
-    read-back and event wait -- plan-cache lookup, forward + merge, eager), and
-    the D2H copy of the output.  Also times the planner on that table: the GPU
-    packer on a cache miss and the fingerprint + lookup on a hit."""
+    (what the vLLM backend calls; it plans on the GPU) with HOST buffers: every
+    step one H2D copy of the step's Q + block table + seq lens (one pinned
+    staging buffer) into the tensors the op reads, the op (device fingerprint of
+    the uploaded table compared on the device -> forward + merge), and the D2H
+    copy of the output.  Timed as the engine runs a decode step -- one CUDA graph
+    of copy + op + copy per step (vLLM full decode graphs) -- and, beside it,
+    eagerly (one Python call per step) and with the table changing every step
+    (re-planned on the device, the first layer of a decode step whose seq lens
+    grew).  Also the planner on that table: the host-synchronising GPU packer
+    (PatDecoder) on a miss and its fingerprint + lookup on a hit."""
     import torch
 
     from paper_2511_22333_b200 import torch_op  # noqa: F401  (registers the op)
@@ -340,10 +344,18 @@ def measure_e2e(P, plan, w, table, q, kc, vc, ws, steps, warmup, dev, flush):
     off_bt = (qb + 255) // 256 * 256
     off_sl = off_bt + (bt.nbytes + 255) // 256 * 256
     nbytes = off_sl + sl.nbytes
-    stage_h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
-    stage_h[:qb].copy_(q.cpu().contiguous().view(-1).view(torch.uint8))
-    stage_h[off_bt:off_bt + bt.nbytes].copy_(torch.from_numpy(np.ascontiguousarray(bt)).view(-1).view(torch.uint8))
-    stage_h[off_sl:off_sl + sl.nbytes].copy_(torch.from_numpy(np.ascontiguousarray(sl)).view(-1).view(torch.uint8))
+
+    def staged(seq):
+        h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        h[:qb].copy_(q.cpu().contiguous().view(-1).view(torch.uint8))
+        h[off_bt:off_bt + bt.nbytes].copy_(torch.from_numpy(np.ascontiguousarray(bt)).view(-1).view(torch.uint8))
+        h[off_sl:off_sl + sl.nbytes].copy_(torch.from_numpy(np.ascontiguousarray(seq)).view(-1).view(torch.uint8))
+        return h
+
+    stage_h = staged(sl)
+    sl2 = sl.copy()
+    sl2[-1] -= 1  # the same batch one token shorter: a different table
+    stage_h2 = staged(sl2)
     stage_d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     qd = stage_d[:qb].view(q.dtype).view(q.shape)
     btd = stage_d[off_bt:off_bt + bt.nbytes].view(torch.int32).view(bt.shape)  # the step's table, as uploaded
@@ -351,15 +363,14 @@ def measure_e2e(P, plan, w, table, q, kc, vc, ws, steps, warmup, dev, flush):
     outh = torch.empty(q.shape, dtype=q.dtype).pin_memory()
     outd = torch.empty_like(q)
     stream = torch.cuda.current_stream(dev)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     op = torch.ops.patb200.decode_attention
 
-    # planner on the uploaded table: GPU packer (miss) and fingerprint + lookup (hit)
+    # planner on the uploaded table through the host-synchronising path
     stage_d.copy_(stage_h)
     torch.cuda.synchronize(dev)
-    dec = P.PatDecoder(q.shape[1], kc.shape[2], q.shape[2], device=dev)
+    hdec = P.PatDecoder(q.shape[1], kc.shape[2], q.shape[2], device=dev)
     t0 = time.perf_counter()
-    mplan = dec.plan_for_device(btd, sld, w.block_size)
+    mplan = hdec.plan_for_device(btd, sld, w.block_size)
     torch.cuda.synchronize(dev)
     miss_ms = (time.perf_counter() - t0) * 1e3
     hits = []
@@ -367,32 +378,47 @@ def measure_e2e(P, plan, w, table, q, kc, vc, ws, steps, warmup, dev, flush):
         btd.add_(0)  # same content, new tensor version: the identity fast path is bypassed
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        assert dec.plan_for_device(btd, sld, w.block_size) is mplan
+        assert hdec.plan_for_device(btd, sld, w.block_size) is mplan
         hits.append((time.perf_counter() - t0) * 1e3)
-    del dec
+    del hdec
 
-    def step(i=None):
-        if i is not None:
-            evs[i][0].record(stream)
-        stage_d.copy_(stage_h, non_blocking=True)
+    def step_body(src):
+        stage_d.copy_(src, non_blocking=True)
         op(qd, kc, vc, btd, sld, outd, 0.0)
         outh.copy_(outd, non_blocking=True)
-        if i is not None:
-            evs[i][1].record(stream)
 
-    for _ in range(warmup):
-        flush.zero_()
-        step()
-    torch.cuda.synchronize(dev)
-    for i in range(steps):
-        flush.zero_()
-        step(i)
-    torch.cuda.synchronize(dev)
-    per = [a.elapsed_time(b) for a, b in evs]
+    def timed(run):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for i in range(warmup):
+            flush.zero_()
+            run(i)
+        torch.cuda.synchronize(dev)
+        for i in range(steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            run(i)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        return float(np.mean([a.elapsed_time(b) for a, b in evs]))
+
+    t_eager = timed(lambda i: step_body(stage_h))
+    graphs = []
+    for src in (stage_h, stage_h2):
+        step_body(src)  # warm-up outside capture (the device decoder exists, tensor maps cached)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs), torch.cuda.graph(g, stream=cs):
+            step_body(src)
+        stream.wait_stream(cs)
+        graphs.append(g)
+    t_graph = timed(lambda i: graphs[0].replay())
+    t_replan = timed(lambda i: graphs[i % 2].replay())
     h2d = qb + bt.nbytes + sl.nbytes  # payload bytes (the staging buffer adds alignment padding only)
     d2h = outh.numel() * outh.element_size()
-    return {"t_ms": float(np.mean(per)), "h2d": h2d, "d2h": d2h, "gpu_packer_miss_ms": miss_ms,
-            "plan_hit_ms": float(np.median(hits))}
+    return {"t_ms": t_graph, "eager_ms": t_eager, "replan_ms": t_replan, "h2d": h2d, "d2h": d2h,
+            "gpu_packer_miss_ms": miss_ms, "plan_hit_ms": float(np.median(hits))}
 
 
 def main():
@@ -487,10 +513,14 @@ def main():
                 "roofline": {"kernel_us": round(tf * 1e3, 2), "achieved": round(gb(tf), 1),
                              "frac": round(gb(tf) / peaks["hbm_gbs"], 4)},
                 "e2e": {"us_per_layer": round(te * 1e3, 2), "value": round(gb(te), 1), "unit": "GB/s",
-                        "h2d_bytes_per_step": r["e2e"]["h2d"], "d2h_bytes_per_step": r["e2e"]["d2h"]},
+                        "h2d_bytes_per_step": r["e2e"]["h2d"], "d2h_bytes_per_step": r["e2e"]["d2h"],
+                        "eager_us_per_layer": round(reduce_max(r["e2e"]["eager_ms"]) * 1e3, 2),
+                        "replan_every_step_us_per_layer": round(reduce_max(r["e2e"]["replan_ms"]) * 1e3, 2)},
                 "planner_ms": {"host_cold": round(r["pack_ms"], 3),
-                               "gpu_packer_miss": round(r["e2e"]["gpu_packer_miss_ms"], 3),
-                               "fingerprint_hit": round(r["e2e"]["plan_hit_ms"], 4)},
+                               "gpu_packer_miss_host_sync": round(r["e2e"]["gpu_packer_miss_ms"], 3),
+                               "fingerprint_hit_host_sync": round(r["e2e"]["plan_hit_ms"], 4),
+                               "device_replan_in_graph": round(
+                                   (reduce_max(r["e2e"]["replan_ms"]) - reduce_max(r["e2e"]["t_ms"])), 4)},
                 "unique_kv_bytes": int(tb), "packs": r["info"].n_packs, "items": r["info"].n_items}
 
     other_summary = {name: summarise(r) for name, r in others.items()}
@@ -538,9 +568,14 @@ def main():
             "e2e": {"value": round(tot_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": main_res["e2e"]["h2d"], "d2h_bytes_per_step": main_res["e2e"]["d2h"],
                     "us_per_layer": round(e2e_ms * 1e3, 2),
-                    "path": "torch.ops.patb200.decode_attention (device fingerprint of the uploaded table, plan-cache "
-                            "hit, forward + merge, eager) with the step's Q + block table + seq lens H2D and the "
-                            "output D2H inside the timed region"},
+                    "eager_us_per_layer": other_summary[args.config]["e2e"]["eager_us_per_layer"],
+                    "replan_every_step_us_per_layer":
+                        other_summary[args.config]["e2e"]["replan_every_step_us_per_layer"],
+                    "path": "torch.ops.patb200.decode_attention, planning on the GPU (device fingerprint of the "
+                            "uploaded table compared on the device, GPU packer + scheduler on a change, forward + "
+                            "merge), the step's Q + block table + seq lens H2D and the output D2H inside the timed "
+                            "region; one CUDA graph of copy + op + copy per step (vLLM full decode graph); eager and "
+                            "re-plan-every-step timings beside it"},
             "gpu_launches": main_res["launches_per_step"] * args.steps,
             "packer_ms_host_cold": round(main_res["pack_ms"], 3),
             "planner_ms": other_summary[args.config]["planner_ms"],
