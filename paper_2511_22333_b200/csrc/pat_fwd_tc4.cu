@@ -179,6 +179,11 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
+// streaming store (evict-first): outputs and partials are read once, by the merge
+__device__ __forceinline__ void st_cs_v4(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ float4 lds_v4f(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // entry ends phase 1; then both lanes claim the other items
       // independently.
       const int n_pair = plan.n_pair[var];
-      bool pair_phase = n_pair > 0;
+      bool pair_phase = n_pair > 0, first_claim = true;
       uint32_t gt = 0, jn = 0, pair_upto = 0;
       for (uint32_t n = 0;; ++n) {
         const uint32_t slot = n & 1;
@@ -357,8 +362,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++jn;
         }
         if (!pair_phase) {
+          // the first claim of every lane is static (lane L of CTA b takes the
+          // (b + L * grid)-th item: no 296-way atomic at kernel start), later
+          // ones come from the counter, offset by the 2 * grid static claims
           int c = 0;
-          if (lane == 0) c = atomicAdd(sched + 2, 1);
+          if (n_pair == 0 && first_claim) c = (int)blockIdx.x + pl * (int)gridDim.x;
+          else if (lane == 0) c = atomicAdd(sched + 2, 1) + (n_pair == 0 ? 2 * (int)gridDim.x : 0);
+          first_claim = false;
           it = n_pair + __shfl_sync(0xffffffffu, c, 0);
           if (it >= n_items) it = -1;
         }
@@ -792,15 +802,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)meta.x * H + head) * D + q * 32);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                  dst[k] = make_uint4(Fmt<T>::pack(f[8 * k] * inv, f[8 * k + 1] * inv),
-                                      Fmt<T>::pack(f[8 * k + 2] * inv, f[8 * k + 3] * inv),
-                                      Fmt<T>::pack(f[8 * k + 4] * inv, f[8 * k + 5] * inv),
-                                      Fmt<T>::pack(f[8 * k + 6] * inv, f[8 * k + 7] * inv));
+                  st_cs_v4(dst + k, make_uint4(Fmt<T>::pack(f[8 * k] * inv, f[8 * k + 1] * inv),
+                                               Fmt<T>::pack(f[8 * k + 2] * inv, f[8 * k + 3] * inv),
+                                               Fmt<T>::pack(f[8 * k + 4] * inv, f[8 * k + 5] * inv),
+                                               Fmt<T>::pack(f[8 * k + 6] * inv, f[8 * k + 7] * inv)));
               } else {
                 float4* dst = reinterpret_cast<float4*>(part_o + ((int64_t)meta.y * H + head) * D + q * 32);
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
-                  dst[k] = make_float4(f[4 * k] * inv, f[4 * k + 1] * inv, f[4 * k + 2] * inv, f[4 * k + 3] * inv);
+                  st_cs_v4(reinterpret_cast<uint4*>(dst + k),
+                           make_uint4(__float_as_uint(f[4 * k] * inv), __float_as_uint(f[4 * k + 1] * inv),
+                                      __float_as_uint(f[4 * k + 2] * inv), __float_as_uint(f[4 * k + 3] * inv)));
               }
             }
           }

@@ -796,7 +796,6 @@ __device__ void ph_schedule(const Sched& S) {
   const Ws& w = S.w;
   const int t = threadIdx.x, nt = blockDim.x;
   __shared__ int s_np, s_err, s_chunk;
-  __shared__ float s_best[32];
   if (t == 0) {
     s_np = *w.npacks;
     s_err = w.err[0];
@@ -1157,6 +1156,7 @@ int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t m
     nsm = 148;
   Dc->num_sms = nsm;
   const int B = max_batch, D = std::min(B, max_blocks + 1) + 1, D1 = D + 1;
+  const size_t Bz = (size_t)B;
   Dc->D = D;
   const size_t BB = (size_t)B * B, BD = (size_t)B * D, BD1 = (size_t)B * D1, N2 = 2 * (size_t)B + 2;
   const int G = Dc->H / Dc->KVH;
@@ -1173,12 +1173,12 @@ int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t m
   dev::Ws& w = Dc->w;
   dev::Sched& S = Dc->S;
   std::vector<F> f = {
-      {(void**)&w.nblk, B * 4}, {(void**)&w.valid, B * 4}, {(void**)&w.err, 8}, {(void**)&w.lcp, BB * 4},
-      {(void**)&w.K, B * 4}, {(void**)&w.hasleaf, B * 4}, {(void**)&w.end, BD * 4}, {(void**)&w.nq, BD * 4},
+      {(void**)&w.nblk, Bz * 4}, {(void**)&w.valid, Bz * 4}, {(void**)&w.err, 8}, {(void**)&w.lcp, BB * 4},
+      {(void**)&w.K, Bz * 4}, {(void**)&w.hasleaf, Bz * 4}, {(void**)&w.end, BD * 4}, {(void**)&w.nq, BD * 4},
       {(void**)&w.minq, BD * 4}, {(void**)&w.term, BD * 4}, {(void**)&w.start, BD1 * 4}, {(void**)&w.stop, BD1 * 4},
       {(void**)&w.span, BD1 * 4}, {(void**)&w.anchor, BD1 * 4}, {(void**)&w.member, BD1 * 4},
-      {(void**)&w.nmemb, B * 4}, {(void**)&w.k0, B * 4}, {(void**)&w.cnt_own, B * 4}, {(void**)&w.pi, B * 4},
-      {(void**)&w.order, B * 4}, {(void**)&w.base, (B + 1) * 4}, {(void**)&w.n_hi, N2 * 4},
+      {(void**)&w.nmemb, Bz * 4}, {(void**)&w.k0, Bz * 4}, {(void**)&w.cnt_own, Bz * 4}, {(void**)&w.pi, Bz * 4},
+      {(void**)&w.order, Bz * 4}, {(void**)&w.base, (Bz + 1) * 4}, {(void**)&w.n_hi, N2 * 4},
       {(void**)&w.n_lo, N2 * 4}, {(void**)&w.n_cnt, N2 * 4}, {(void**)&w.n_depth, N2 * 4},
       {(void**)&w.n_rep, N2 * 4}, {(void**)&w.n_a0, N2 * 4}, {(void**)&w.n_a1, N2 * 4},
       {(void**)&w.n_span, N2 * 4}, {(void**)&w.n_pack, N2 * 4}, {(void**)&w.npacks, 4},
@@ -1188,9 +1188,9 @@ int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t m
       {(void**)&S.unit_pack, cap_units * 4}, {(void**)&S.unit_page0, cap_units * 4},
       {(void**)&S.unit_ntok, cap_units * 4}, {(void**)&S.unit_slot_off, (cap_units + 1) * 4},
       {(void**)&S.unit_slot, cap_members * 4}, {(void**)&S.items, cap_items_c * sizeof(Item)},
-      {(void**)&S.n_items, 16}, {(void**)&S.n_pair, 16}, {(void**)&S.merge_desc, B * 16},
+      {(void**)&S.n_items, 16}, {(void**)&S.n_pair, 16}, {(void**)&S.merge_desc, Bz * 16},
       {(void**)&S.n_merge, 4}, {(void**)&S.parts, N2 * 4}, {(void**)&S.ubase, (N2 + 1) * 4},
-      {(void**)&S.qcnt, B * 4}, {(void**)&S.qoff, B * 4}, {(void**)&S.qlist_n, B * 4},
+      {(void**)&S.qcnt, Bz * 4}, {(void**)&S.qoff, Bz * 4}, {(void**)&S.qlist_n, Bz * 4},
       {(void**)&S.qlist, BD1 * 8}, {(void**)&S.prior, BD1 * 4}, {(void**)&S.ukey, P2 * 8},
       {(void**)&Dc->h_new, 8}, {(void**)&Dc->h_old, 8}, {(void**)&Dc->run, 4}, {(void**)&Dc->nrun, 4},
       {(void**)&Dc->bar, 8}};

@@ -15,7 +15,8 @@ from paper_2511_22333_b200 import configs  # noqa: E402
 
 
 def main(names):
-    buf = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    import bench
+    buf = bench.L2Flush("cuda")
     for name in names:
         w = configs.workload(name)
         g = torch.Generator(device="cuda").manual_seed(0)
@@ -29,7 +30,7 @@ def main(names):
                                     pair_items=os.environ.get("PAT_AB_PAIR") == "1")
         gr = P.PatLayerGraph(plan, q, kc, vc)
         ts = []
-        for i in range(33):
+        for i in range(43):
             buf.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
