@@ -240,6 +240,17 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int ab_fmt, int a
          ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 __device__ __forceinline__ uint16_t bits16(uint32_t packed_lo) { return (uint16_t)(packed_lo & 0xffffu); }
+// shared-memory descriptor of an MN-major operand 16 elements (32 B) wide,
+// SWIZZLE_32B (layout type 6): 8-row K groups 256 B apart (SBO)
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((256u >> 4) & 0x3FFF) << 16;  // LBO (one atom along N: unused)
+  d |= (uint64_t)((256u >> 4) & 0x3FFF) << 32;  // SBO
+  d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
+  d |= (uint64_t)6 << 61;                        // SWIZZLE_32B
+  return d;
+}
 
 __device__ __forceinline__ Item load_item(const Item* p) {
   const int4* q = reinterpret_cast<const int4*>(p);
@@ -465,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
       constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
       constexpr uint32_t idesc_qkn = idesc_f16(kM, kNarrow, Fmt<T>::ab, 0, 0);  // S^T = K Q^T
-      constexpr uint32_t idesc_pvn = idesc_f16(kM, kNarrow, Fmt<T>::ab, 1, 0);  // O^T = V^T P^T
+      constexpr uint32_t idesc_pvn = idesc_f16(kM, kNarrow, Fmt<T>::ab, 1, 1);  // O^T = V^T P^T
       uint32_t tcnt = 0, rpos = 0, qu = 0, ou = 0;
       for (uint32_t n = 0;; ++n) {
         mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1);
@@ -537,10 +548,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int nk = (vt + 15) / 16;
               for (int j = 0; j < nk; ++j) {
                 const uint64_t ad = umma_desc_sw128(sV(src, s) + (uint32_t)(j * 16 * 128), L::kPlane, 1024);
-                umma_f16_ss(tg + 128u, ad, umma_desc_sw128(sPn(b, 0) + (uint32_t)(j * 32), 16, 1024), idesc_pvn,
+                umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 0) + (uint32_t)(j * 512)), idesc_pvn,
                             (t == 0 && j == 0) ? 0u : 1u);
                 if constexpr (kSplit)
-                  umma_f16_ss(tg + 128u, ad, umma_desc_sw128(sPn(b, 1) + (uint32_t)(j * 32), 16, 1024), idesc_pvn,
+                  umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 1) + (uint32_t)(j * 512)), idesc_pvn,
                               1u);
               }
               umma_commit(bar(SP_FREE + b));
@@ -888,22 +899,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar_sync(nbar, 128);  // exchange slots read before they are reused
           }
           if (tw) {
-            // P^T[r][token] into the K-major 128B-swizzled B operand (16 rows x 64 tokens)
-            const uint32_t toff = (uint32_t)((ln & 7) * 2);
+            // P^T into the MN-major 32B-swizzled B operand ([64 tokens][16 rows] x 2 B):
+            // this thread's token row is 32 contiguous bytes, two 16-byte stores
+            // (hi, and lo for bf16) instead of 16 scattered 2-byte ones
+            uint32_t ph[kNarrow / 2], pq[kNarrow / 2];
 #pragma unroll
-            for (int r = 0; r < kNarrow; ++r) {
-              const float mu = m_ref[r] == -INFINITY ? 0.f : m_ref[r];
-              const float p = ex2_approx(x[r] - mu);
-              const uint32_t hp = Fmt<T>::pack(p, 0.f);
-              const uint32_t a = (uint32_t)(r * 128 + ((((ln >> 3) ^ (r & 7))) << 4)) + toff;
-              sts_u16(sPn(b, 0) + a, bits16(hp));
+            for (int r = 0; r < kNarrow; r += 2) {
+              const float mu0 = m_ref[r] == -INFINITY ? 0.f : m_ref[r];
+              const float mu1 = m_ref[r + 1] == -INFINITY ? 0.f : m_ref[r + 1];
+              const float p0 = ex2_approx(x[r] - mu0), p1 = ex2_approx(x[r + 1] - mu1);
+              ph[r / 2] = Fmt<T>::pack(p0, p1);
+              const float2 hv = Fmt<T>::unpack(ph[r / 2]);
               if constexpr (kSplit) {
-                const float hv = Fmt<T>::unpack(hp).x;
-                sts_u16(sPn(b, 1) + a, bits16(Fmt<T>::pack(p - hv, 0.f)));
-                lsum[r] += p;
+                pq[r / 2] = Fmt<T>::pack(p0 - hv.x, p1 - hv.y);
+                lsum[r] += p0;
+                lsum[r + 1] += p1;
               } else {
-                lsum[r] += Fmt<T>::unpack(hp).x;
+                lsum[r] += hv.x;
+                lsum[r + 1] += hv.y;
               }
+            }
+            const uint32_t sw = (uint32_t)((ln >> 2) & 1);  // 32B swizzle: 16-byte chunk ^= bit 7 of the address
+            const uint32_t a0 = (uint32_t)(ln * 32) + (sw << 4), a1 = (uint32_t)(ln * 32) + ((sw ^ 1u) << 4);
+            st_shared_v4(sPn(b, 0) + a0, make_uint4(ph[0], ph[1], ph[2], ph[3]));
+            st_shared_v4(sPn(b, 0) + a1, make_uint4(ph[4], ph[5], ph[6], ph[7]));
+            if constexpr (kSplit) {
+              st_shared_v4(sPn(b, 1) + a0, make_uint4(pq[0], pq[1], pq[2], pq[3]));
+              st_shared_v4(sPn(b, 1) + a1, make_uint4(pq[4], pq[5], pq[6], pq[7]));
             }
           }
           if (vt < kNN && (vt % kN) != 0) zero_v_tail(pl, s0, vt);
