@@ -76,6 +76,38 @@ struct Ws {
   int32_t* p_partial;
 };
 
+// Exclusive prefix sum of one value per thread over the block (blockDim a
+// multiple of 32, <= 1024): warp shuffles, then the 32 warp totals.  All
+// threads must call it; *total gets the block sum.
+__device__ __forceinline__ int block_excl_scan(int v, int* total) {
+  __shared__ int wsum[32];
+  __shared__ int s_total;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int z = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < nw) wsum[lane] = z;  // inclusive over warps
+    if (lane == 31) s_total = z;
+  }
+  __syncthreads();
+  const int r = x - v + (wid > 0 ? wsum[wid - 1] : 0);
+  *total = s_total;
+  __syncthreads();
+  return r;
+}
+
 __device__ __forceinline__ int tok_at(const Ws& w, int q, int p) { return p == w.nblk[q] - 1 ? w.valid[q] : w.bs; }
 __device__ __forceinline__ int blk_at(const Ws& w, int q, int p) { return w.bt[(int64_t)q * w.stride + p]; }
 
@@ -197,48 +229,73 @@ __device__ void ph_levels(const Ws& w, unsigned long long* skey) {
       }
       __syncthreads();
     }
-  // serial pass over the (few) entries by one thread keeps this simple and exact
-  if (threadIdx.x == 0) {
-    int M = 0;
-    while (M < w.B && skey[M] != ~0ull) ++M;
-    int Kq = 0;
-    const int nbq = w.nblk[q];
-    int sufmin = q;
-    // distinct lcp values front to back (ascending): one internal level each
-    int i = 0;
-    while (i < M) {
+  // The sorted entries (lcp value v, query r) group into levels, one per
+  // distinct v (ascending).  Everything per level is a parallel scan over the
+  // entries: level index (inclusive count of group starts), members at or past
+  // the level (M - start + 1), terminal members (r ends exactly at v, summed
+  // per level) and the smallest member id (suffix minimum of r from the start).
+  int32_t* tflag = reinterpret_cast<int32_t*>(skey + P);  // [P] terminal flag
+  int32_t* lvl = tflag + P;                              // [P] level index (scan)
+  int32_t* suf = lvl + P;                                // [P] suffix min of r
+  int32_t* tcnt = suf + P;                               // [P] terminal count per level
+  __shared__ int s_m;
+  if (threadIdx.x == 0) s_m = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const unsigned long long k = skey[i];
+    const bool valid = k != ~0ull;
+    const int v = (int)(k >> 32);
+    tflag[i] = valid && w.nblk[(int)(k & 0xffffffffu)] == v;
+    lvl[i] = valid && (i == 0 || (int)(skey[i - 1] >> 32) != v);
+    suf[i] = valid ? (int)(k & 0xffffffffu) : 0x7fffffff;
+    tcnt[i] = 0;
+    if (valid) atomicAdd(&s_m, 1);
+  }
+  __syncthreads();
+  const int M = s_m;
+  for (int off = 1; off < P; off <<= 1) {  // inclusive scan (levels), suffix min (members)
+    int a[4], m[4];
+    int n = 0;
+    for (int i = threadIdx.x; i < P; i += blockDim.x, ++n) {
+      if (n < 4) {
+        a[n] = i >= off ? lvl[i - off] : 0;
+        m[n] = i + off < P ? suf[i + off] : 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    n = 0;
+    for (int i = threadIdx.x; i < P; i += blockDim.x, ++n) {
+      if (n < 4) {
+        lvl[i] += a[n];
+        suf[i] = min(suf[i], m[n]);
+      }
+    }
+    __syncthreads();
+  }
+  const int Kq = M > 0 ? lvl[M - 1] : 0;
+  const bool over = Kq > w.D;
+  const int nbq = w.nblk[q];
+  for (int i = threadIdx.x; i < M; i += blockDim.x)
+    if (tflag[i]) atomicAdd(&tcnt[lvl[i] - 1], 1);
+  __syncthreads();
+  if (over) {
+    if (threadIdx.x == 0 && atomicCAS(&w.err[0], 0, PAT_ERR_NO_FEASIBLE_CONFIG) == 0) w.err[1] = q;
+  } else {
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
       const int v = (int)(skey[i] >> 32);
-      int j = i;
-      int tcount = 0;
-      while (j < M && (int)(skey[j] >> 32) == v) {
-        const int r = (int)(skey[j] & 0xffffffffu);
-        if (w.nblk[r] == v) ++tcount;
-        ++j;
-      }
-      if (Kq >= w.D) {
-        if (atomicCAS(&w.err[0], 0, PAT_ERR_NO_FEASIBLE_CONFIG) == 0) w.err[1] = q;
-        M = -1;  // abandon this query (the plan is rejected)
-        break;
-      }
-      w.end[(int64_t)q * w.D + Kq] = v;
-      w.nq[(int64_t)q * w.D + Kq] = 1 + (M - i);
-      w.term[(int64_t)q * w.D + Kq] = tcount + (nbq == v ? 1 : 0);
-      w.minq[(int64_t)q * w.D + Kq] = i;  // placeholder: group start, resolved below
-      ++Kq;
-      i = j;
-    }
-    // resolve minimum member of {r : lcp >= end_k} u {q} via a backward suffix min
-    if (M < 0) Kq = 0, M = 0;
-    int k = Kq - 1;
-    for (int e = M - 1; e >= 0 && k >= 0; --e) {
-      sufmin = min(sufmin, (int)(skey[e] & 0xffffffffu));
-      while (k >= 0 && w.minq[(int64_t)q * w.D + k] == e) {
-        w.minq[(int64_t)q * w.D + k] = sufmin;
-        --k;
+      if (i == 0 || (int)(skey[i - 1] >> 32) != v) {  // the first entry of level k
+        const int k = lvl[i] - 1;
+        w.end[(int64_t)q * w.D + k] = v;
+        w.nq[(int64_t)q * w.D + k] = 1 + (M - i);
+        w.term[(int64_t)q * w.D + k] = tcnt[k] + (nbq == v ? 1 : 0);
+        w.minq[(int64_t)q * w.D + k] = min(q, suf[i]);
       }
     }
-    w.K[q] = Kq;
-    w.hasleaf[q] = (Kq == 0) || w.end[(int64_t)q * w.D + Kq - 1] < nbq;
+  }
+  if (threadIdx.x == 0) {
+    const int K = over ? 0 : Kq;
+    w.K[q] = K;
+    w.hasleaf[q] = K == 0 || (int)(skey[M - 1] >> 32) < nbq;
   }
   __syncthreads();
   }
@@ -348,24 +405,13 @@ __global__ void k_rank(Ws w) {
 // single CTA exclusive scan of cnt_own -> base
 __device__ void ph_scan_nodes(const Ws& w) {
   if (blockIdx.x != 0) return;  // one CTA of up to 1024 threads
-  __shared__ int32_t part[1024];
   const int t = threadIdx.x, n = w.B;
   const int per = (n + blockDim.x - 1) / blockDim.x;
   int s = 0;
   for (int i = t * per; i < min(n, (t + 1) * per); ++i) s += w.cnt_own[i];
-  part[t] = s;
-  __syncthreads();
-  if (t == 0) {
-    int acc = 0;
-    for (int i = 0; i < (int)blockDim.x; ++i) {
-      int v = part[i];
-      part[i] = acc;
-      acc += v;
-    }
-    w.base[n] = acc;
-  }
-  __syncthreads();
-  int acc = part[t];
+  int total;
+  int acc = block_excl_scan(s, &total);
+  if (t == 0) w.base[n] = total;
   for (int i = t * per; i < min(n, (t + 1) * per); ++i) {
     w.base[i] = acc;
     acc += w.cnt_own[i];
@@ -421,16 +467,22 @@ __global__ void k_nodes(Ws w) {
 }
 
 // thread per node: rank among emitting nodes by (hi asc, depth desc)
-__device__ void ph_order(const Ws& w) {
+__device__ void ph_order(const Ws& w, int4* snode, int cap) {
   const int N = w.base[w.B];
+  // (hi, depth, emitting) of every node, staged once per CTA when it fits
+  const bool st = N <= cap;
+  if (st) {
+    for (int j = threadIdx.x; j < N; j += blockDim.x) snode[j] = make_int4(w.n_hi[j], w.n_depth[j], w.n_cnt[j] > 0, 0);
+    __syncthreads();
+  }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     if (w.n_cnt[i] == 0) continue;
     const int hi = w.n_hi[i], dp = w.n_depth[i];
     int r = 0;
     for (int j = 0; j < N; ++j) {
-      if (j == i || w.n_cnt[j] == 0) continue;
-      const int hj = w.n_hi[j], dj = w.n_depth[j];
-      r += (hj < hi) || (hj == hi && dj > dp);
+      const int4 nj = st ? snode[j] : make_int4(w.n_hi[j], w.n_depth[j], w.n_cnt[j] > 0, 0);
+      if (j == i || !nj.z) continue;
+      r += (nj.x < hi) || (nj.x == hi && nj.y > dp);
     }
     w.n_pack[i] = r;
     w.p_node[r] = i;
@@ -439,20 +491,25 @@ __device__ void ph_order(const Ws& w) {
 }
 __global__ void k_order(Ws w) {
   if (w.run && !*w.run) return;
-  ph_order(w);
+  ph_order(w, nullptr, 0);
 }
 
 // single thread: query offsets per pack (packs <= 2B)
+// CTA 0: exclusive scan of the packs' member counts (any block size)
 __device__ void ph_pack_offsets(const Ws& w) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  const int np = *w.npacks;
-  int acc = 0;
-  for (int p = 0; p < np; ++p) {
+  if (blockIdx.x != 0) return;
+  const int np = *w.npacks, t = threadIdx.x, nt = blockDim.x;
+  const int per = (np + nt - 1) / nt;
+  int sum = 0;
+  for (int p = t * per; p < min(np, (t + 1) * per); ++p) sum += w.n_cnt[w.p_node[p]];
+  int total;
+  int acc = block_excl_scan(sum, &total);
+  if (t == 0) w.p_qoff[np] = total;
+  for (int p = t * per; p < min(np, (t + 1) * per); ++p) {
     w.p_qoff[p] = acc;
     acc += w.n_cnt[w.p_node[p]];
     w.p_partial[p] = 0;
   }
-  w.p_qoff[np] = acc;
 }
 __global__ void k_pack_offsets(Ws w) {
   if (w.run && !*w.run) return;
@@ -552,14 +609,15 @@ int device_pack(const int32_t* d_bt, int64_t stride, const int32_t* d_seq, int B
   }
   int PB = 1;
   while (PB < B) PB <<= 1;
-  dev::k_levels<<<B, 256, PB * 8, st>>>(w);
+  if (PB * 24 > 48 * 1024) cudaFuncSetAttribute(dev::k_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, PB * 24);
+  dev::k_levels<<<B, 1024, PB * 24, st>>>(w);
   dev::k_decide<<<gq, TB, 0, st>>>(w);
   dev::k_rank<<<(B * 32 + 255) / 256, 256, 0, st>>>(w);
   dev::k_scan_nodes<<<1, 1024, 0, st>>>(w);
   dev::k_nodes_init<<<64, 256, 0, st>>>(w);
   dev::k_nodes<<<gq, TB, 0, st>>>(w);
   dev::k_order<<<64, 256, 0, st>>>(w);
-  dev::k_pack_offsets<<<1, 1, 0, st>>>(w);
+  dev::k_pack_offsets<<<1, 1024, 0, st>>>(w);
   dev::k_members<<<gq, TB, 0, st>>>(w);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -755,33 +813,18 @@ struct Sched {
 // exclusive scan over n values produced by `val(i)` with one CTA; returns the total
 template <typename F, typename O>
 __device__ int cta_scan(int n, F val, O put) {
-  __shared__ int part[1024];
-  __shared__ int total;
   const int t = threadIdx.x, nt = blockDim.x;
   const int per = (n + nt - 1) / nt;
   int s = 0;
   for (int i = t * per; i < min(n, (t + 1) * per); ++i) s += val(i);
-  part[t] = s;
-  __syncthreads();
-  if (t == 0) {
-    int acc = 0;
-    for (int i = 0; i < nt; ++i) {
-      const int v = part[i];
-      part[i] = acc;
-      acc += v;
-    }
-    total = acc;
-  }
-  __syncthreads();
-  int acc = part[t];
+  int total;
+  int acc = block_excl_scan(s, &total);
   for (int i = t * per; i < min(n, (t + 1) * per); ++i) {
     put(i, acc);
     acc += val(i);
   }
   __syncthreads();
-  const int r = total;
-  __syncthreads();
-  return r;
+  return total;
 }
 
 __device__ __forceinline__ float sched_item_ns(const Sched& S, int rows, int ntok) {
@@ -791,8 +834,24 @@ __device__ __forceinline__ float sched_item_ns(const Sched& S, int rows, int nto
 
 // One CTA: split (chunk chosen by a makespan estimate over the lanes), units,
 // partial slots in unit order, longest-first work items, merge descriptors.
-__device__ void ph_schedule(const Sched& S) {
+#ifdef PAT_TC_TRACE
+__device__ long long g_sched_stamp[16];
+#define SCHED_STAMP(i)                                        \
+  do {                                                        \
+    if (threadIdx.x == 0) {                                   \
+      long long t_;                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));  \
+      g_sched_stamp[i] = t_;                                  \
+    }                                                         \
+  } while (0)
+#else
+#define SCHED_STAMP(i) \
+  do {                 \
+  } while (0)
+#endif
+__device__ void ph_schedule(const Sched& S, uint8_t* smem, int smem_bytes) {
   if (blockIdx.x != 0) return;  // one CTA of 1024 threads
+  SCHED_STAMP(0);
   const Ws& w = S.w;
   const int t = threadIdx.x, nt = blockDim.x;
   __shared__ int s_np, s_err, s_chunk;
@@ -808,9 +867,20 @@ __device__ void ph_schedule(const Sched& S) {
     return;
   }
   auto pk_node = [&](int p) { return w.p_node[p]; };
-  auto pk_pages = [&](int p) { const int id = pk_node(p); return w.n_a1[id] - w.n_a0[id]; };
-  auto pk_rows = [&](int p) { return (w.p_qoff[p + 1] - w.p_qoff[p]) * S.G; };
-  auto pk_kv = [&](int p) { return w.n_span[pk_node(p)]; };
+  // per-pack (pages, rows, kv) staged in shared memory when it fits (every
+  // phase below reads them many times)
+  int3* spk = reinterpret_cast<int3*>(smem);
+  const bool pk_smem = NP * (int)sizeof(int3) <= smem_bytes;
+  if (pk_smem) {
+    for (int p = t; p < NP; p += nt) {
+      const int id = pk_node(p);
+      spk[p] = make_int3(w.n_a1[id] - w.n_a0[id], (w.p_qoff[p + 1] - w.p_qoff[p]) * S.G, w.n_span[id]);
+    }
+    __syncthreads();
+  }
+  auto pk_pages = [&](int p) { if (pk_smem) return spk[p].x; const int id = pk_node(p); return w.n_a1[id] - w.n_a0[id]; };
+  auto pk_rows = [&](int p) { return pk_smem ? spk[p].y : (w.p_qoff[p + 1] - w.p_qoff[p]) * S.G; };
+  auto pk_kv = [&](int p) { return pk_smem ? spk[p].z : w.n_span[pk_node(p)]; };
 
   // pack spans: the rep query's row [a0, a1)
   const int nblk = cta_scan(NP, pk_pages, [&](int i, int v) { S.pack_blk_off[i] = v; });
@@ -823,6 +893,7 @@ __device__ void ph_schedule(const Sched& S) {
       if (o + j < S.cap_blk) S.pack_blk[o + j] = w.bt[(int64_t)rep * w.stride + a0 + j];
   }
 
+  SCHED_STAMP(1);
   // chunk (pages, power of two): minimise the makespan estimate
   // over the candidates whose units, member slots and items fit the capacities
   int maxp = 1;
@@ -863,12 +934,23 @@ __device__ void ph_schedule(const Sched& S) {
         memb += parts * (rows / S.G);
         its += parts * rb * S.KVH;
       }
-      atomicAdd(&s_work, work);
-      atomicAdd(&s_bytes, bytes);
-      atomicMax((int*)&s_worst, __float_as_int(worst));  // non-negative floats order as ints
-      atomicAdd(&s_units, units);
-      atomicAdd(&s_memb, memb);
-      atomicAdd(&s_items, its);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {  // warp sums first: one shared atomic per warp
+        work += __shfl_xor_sync(0xffffffffu, work, o);
+        bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+        worst = fmaxf(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+        units += __shfl_xor_sync(0xffffffffu, units, o);
+        memb += __shfl_xor_sync(0xffffffffu, memb, o);
+        its += __shfl_xor_sync(0xffffffffu, its, o);
+      }
+      if ((t & 31) == 0) {
+        atomicAdd(&s_work, work);
+        atomicAdd(&s_bytes, bytes);
+        atomicMax((int*)&s_worst, __float_as_int(worst));  // non-negative floats order as ints
+        atomicAdd(&s_units, units);
+        atomicAdd(&s_memb, memb);
+        atomicAdd(&s_items, its);
+      }
       __syncthreads();
       const float mean = s_items > 0 ? s_work / s_items : 0.f;
       const float est = fmaxf(s_bytes / S.hbm_bpns, fmaxf(s_work / S.lanes, s_worst) + 0.5f * mean);
@@ -886,6 +968,7 @@ __device__ void ph_schedule(const Sched& S) {
   }
   const int chunk = s_chunk;
 
+  SCHED_STAMP(2);
   // units: pack p -> parts[p] near-equal page runs, larger first, the last
   // carrying the partial block (simulator.py:137-154)
   for (int p = t; p < NP; p += nt) S.parts[p] = (pk_pages(p) + chunk - 1) / chunk;
@@ -910,6 +993,7 @@ __device__ void ph_schedule(const Sched& S) {
                           [&](int i, int v) { S.unit_slot_off[i] = v; });
   if (t == 0) S.unit_slot_off[NU] = NM;
 
+  SCHED_STAMP(3);
   // slots: a query covered by more than one unit gets one slot per unit, in
   // unit order (the reference fold order, attention.py:228-235)
   for (int q = t; q < w.B; q += nt) S.qcnt[q] = 0, S.qlist_n[q] = 0;
@@ -956,10 +1040,15 @@ __device__ void ph_schedule(const Sched& S) {
   }
   __syncthreads();
 
+  SCHED_STAMP(4);
   // work items (unit x 128-row block x kv head), longest (estimated) first:
   // units sorted by cost, descending (bitonic sort over the units in global memory)
   int P2 = 1;
   while (P2 < NU) P2 <<= 1;
+  // the sort keys in shared memory (after the pack records) when they fit
+  const int koff = pk_smem ? ((NP * (int)sizeof(int3) + 15) & ~15) : 0;
+  unsigned long long* ukey =
+      koff + P2 * 8 <= smem_bytes ? reinterpret_cast<unsigned long long*>(smem + koff) : S.ukey;
   for (int u = t; u < P2; u += nt) {
     unsigned long long key = ~0ull;
     if (u < NU) {
@@ -967,7 +1056,7 @@ __device__ void ph_schedule(const Sched& S) {
       const float c = sched_item_ns(S, min(pk_rows(p), 128), S.unit_ntok[u]) * ((pk_rows(p) + 127) / 128);
       key = ((unsigned long long)(0xFFFFFFFFu - (unsigned)fminf(c, 4.0e9f)) << 32) | (unsigned)u;
     }
-    S.ukey[u] = key;
+    ukey[u] = key;
   }
   __syncthreads();
   for (int k = 2; k <= P2; k <<= 1)
@@ -976,17 +1065,18 @@ __device__ void ph_schedule(const Sched& S) {
         const int l = i ^ j;
         if (l > i) {
           const bool up = (i & k) == 0;
-          const unsigned long long a = S.ukey[i], b = S.ukey[l];
-          if ((a > b) == up) S.ukey[i] = b, S.ukey[l] = a;
+          const unsigned long long a = ukey[i], b = ukey[l];
+          if ((a > b) == up) ukey[i] = b, ukey[l] = a;
         }
       }
       __syncthreads();
     }
+  SCHED_STAMP(5);
   const int NI = cta_scan(NU, [&](int r) {
-    const int u = (int)(S.ukey[r] & 0xFFFFFFFFu);
+    const int u = (int)(ukey[r] & 0xFFFFFFFFu);
     return ((pk_rows(S.unit_pack[u]) + 127) / 128) * S.KVH;
   }, [&](int r, int v) {
-    const int u = (int)(S.ukey[r] & 0xFFFFFFFFu), p = S.unit_pack[u], rows = pk_rows(p);
+    const int u = (int)(ukey[r] & 0xFFFFFFFFu), p = S.unit_pack[u], rows = pk_rows(p);
     int k = v;
     for (int r0 = 0; r0 < rows; r0 += 128)
       for (int h = 0; h < S.KVH; ++h, ++k)
@@ -997,10 +1087,7 @@ __device__ void ph_schedule(const Sched& S) {
     S.n_items[t] = t == VAR_TC ? NI : 0;
     S.n_pair[t] = 0;
   }
-}
-__global__ void __launch_bounds__(1024) k_schedule(Sched S) {
-  if (S.w.run && !*S.w.run) return;
-  ph_schedule(S);
+  SCHED_STAMP(6);
 }
 
 // grid barrier of the persistent planner (every CTA resident: cooperative
@@ -1042,6 +1129,22 @@ __device__ void ph_hash(const int32_t* __restrict__ bt, int64_t stride, const in
   if (lane == 0 && acc) atomicAdd(acc_out, (unsigned long long)acc);
 }
 
+#ifdef PAT_TC_TRACE
+__device__ long long g_plan_stamp[32];
+#define PLAN_STAMP(i)                                                        \
+  do {                                                                       \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                               \
+      long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+      g_plan_stamp[i] = t_;                                                  \
+    }                                                                        \
+  } while (0)
+#else
+#define PLAN_STAMP(i) \
+  do {                \
+  } while (0)
+#endif
+
 struct PlanState {
   unsigned long long* h_acc;  // fingerprint accumulator (left at 0 between calls)
   unsigned long long* h_old;  // fingerprint of the planned table
@@ -1053,10 +1156,11 @@ struct PlanState {
 // The whole planner in ONE launch: fingerprint -> compare -> (only when the
 // table changed) reset, rows, duplicates, pairwise prefixes, levels, decisions,
 // DFS rank, nodes, pack order and members, then the schedule on CTA 0.
-__global__ void __launch_bounds__(1024, 1) k_plan(Ws w, Sched S, PlanState ps, int N2) {
+__global__ void __launch_bounds__(1024, 1) k_plan(Ws w, Sched S, PlanState ps, int N2, int dyn_bytes) {
   extern __shared__ __align__(16) uint8_t dsm[];
   ph_hash(w.bt, w.stride, w.seq, w.B, w.bs, ps.h_acc);
   grid_sync(ps.bar);
+  PLAN_STAMP(0);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long h = *ps.h_acc +
         (((unsigned long long)(unsigned)w.B << 32) ^ (unsigned long long)(unsigned)w.bs ^ 0x7A7A000000000000ull);
@@ -1069,6 +1173,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan(Ws w, Sched S, PlanState ps, i
     }
   }
   grid_sync(ps.bar);
+  PLAN_STAMP(1);
   if (!*(volatile int32_t*)ps.run) return;
   {
     const int BD1 = w.B * (w.D + 1);
@@ -1077,35 +1182,57 @@ __global__ void __launch_bounds__(1024, 1) k_plan(Ws w, Sched S, PlanState ps, i
     if (blockIdx.x == 0 && threadIdx.x == 0) w.err[0] = w.err[1] = *w.npacks = 0;
   }
   grid_sync(ps.bar);
+  PLAN_STAMP(2);
   ph_rows(w);
   grid_sync(ps.bar);
+  PLAN_STAMP(3);
   ph_dup(w, (int32_t*)dsm);
   grid_sync(ps.bar);
+  PLAN_STAMP(4);
   ph_lcp(w);
   grid_sync(ps.bar);
+  PLAN_STAMP(5);
   ph_levels(w, (unsigned long long*)dsm);
   grid_sync(ps.bar);
+  PLAN_STAMP(6);
   ph_decide(w);
   grid_sync(ps.bar);
+  PLAN_STAMP(7);
   ph_rank(w);
   grid_sync(ps.bar);
+  PLAN_STAMP(8);
   ph_scan_nodes(w);
   grid_sync(ps.bar);
+  PLAN_STAMP(9);
   ph_nodes_init(w);
   grid_sync(ps.bar);
+  PLAN_STAMP(10);
   ph_nodes(w);
   grid_sync(ps.bar);
-  ph_order(w);
+  PLAN_STAMP(11);
+  ph_order(w, reinterpret_cast<int4*>(dsm), dyn_bytes / 16);
   grid_sync(ps.bar);
+  PLAN_STAMP(12);
   ph_pack_offsets(w);
   grid_sync(ps.bar);
+  PLAN_STAMP(13);
   ph_members(w);
   grid_sync(ps.bar);
-  ph_schedule(S);
+  PLAN_STAMP(14);
+  ph_schedule(S, dsm, dyn_bytes);
+  __syncthreads();
+  PLAN_STAMP(15);
 }
 
 }  // namespace dev
 }  // namespace pat
+
+// dynamic shared memory of the planner kernel: the largest phase need (row
+// sort, per-query key sort + flags, node records, pack records + unit keys)
+static int plan_smem(int P, int PB, int n2) {
+  const int want = std::max({P * 4, PB * 24, n2 * 16, n2 * 12 + 8 * 4096});
+  return std::min(want, 190 * 1024);
+}
 
 struct pat_decoder {
   int Bmax = 0, maxb = 0, bs = 16, H = 0, KVH = 0, d = 0, D = 0, num_sms = 148, device = -1;
@@ -1214,7 +1341,7 @@ int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t m
     while (P < std::max(B, max_blocks)) P <<= 1;
     int PB = 1;
     while (PB < B) PB <<= 1;
-    const int dyn = std::max(P * 4, PB * 8);
+    const int dyn = plan_smem(P, PB, 2 * B + 2);
     cudaFuncSetAttribute(dev::k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_plan, 1024, dyn);
@@ -1337,10 +1464,10 @@ int pat_decoder_forward(pat_decoder* Dc, const int32_t* block_tables, int64_t bt
     while (P < std::max(B, max_blocks)) P <<= 1;
     int PB = 1;
     while (PB < B) PB <<= 1;
-    const int dyn = std::max(P * 4, PB * 8);
+    const int dyn = plan_smem(P, PB, 2 * Dc->Bmax + 2);
     dev::PlanState ps{Dc->h_new, Dc->h_old, Dc->run, Dc->nrun, Dc->bar};
-    int n2 = N2;
-    void* args[] = {(void*)&w, (void*)&S, (void*)&ps, (void*)&n2};
+    int n2 = N2, dynb = dyn;
+    void* args[] = {(void*)&w, (void*)&S, (void*)&ps, (void*)&n2, (void*)&dynb};
     cudaError_t le = cudaLaunchCooperativeKernel((const void*)dev::k_plan, dim3(Dc->plan_grid), dim3(1024), args,
                                                  (size_t)dyn, st);
     if (le != cudaSuccess) {
@@ -1398,6 +1525,14 @@ void pat_decoder_destroy(pat_decoder* Dc) {
 //  what: 0 npacks[1] 1 p_qoff 2 p_q 3 pack_blk_off 4 pack_blk 5 unit_pack 6 unit_page0
 //        7 unit_ntok 8 unit_slot_off 9 unit_slot 10 items (8 ints each) 11 n_items[4]
 //        12 merge_desc (4 ints each) 13 n_merge[1] 14 p_node 15 parts
+#ifdef PAT_TC_TRACE
+extern "C" int pat_debug_plan_stamps(long long* host) {
+  int e = (int)cudaMemcpyFromSymbol(host, pat::dev::g_plan_stamp, sizeof(pat::dev::g_plan_stamp));
+  if (!e) e = (int)cudaMemcpyFromSymbol(host + 32, pat::dev::g_sched_stamp, sizeof(pat::dev::g_sched_stamp));
+  return e;
+}
+#endif
+
 extern "C" int pat_decoder_debug_export(pat_decoder* Dc, int32_t what, int32_t* host, int64_t n_ints) {
   if (!Dc || !host) return PAT_ERR_INVALID_SPEC;
   const void* src = nullptr;
