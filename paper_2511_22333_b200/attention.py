@@ -186,10 +186,13 @@ class PatDeviceDecoder:
     def fits(self, block_tables) -> bool:
         return block_tables.shape[0] <= self.max_batch and block_tables.shape[1] <= self.max_blocks
 
-    def forward(self, block_tables, seq_lens, q, k_cache, v_cache, out=None, scale=None, stream=None):
+    def forward(self, block_tables, seq_lens, q, k_cache, v_cache, out=None, scale=None, stream=None,
+                same_table=None):
         """Every layer of a decode step passes the same (unmodified) table tensors:
         those calls skip even the device fingerprint (tensor identity + autograd
-        version counter, the PAT_DECODE_SAME_TABLE flag)."""
+        version counter, the PAT_DECODE_SAME_TABLE flag).  ``same_table=True``
+        asserts it explicitly (the table is the one the previous call planned);
+        ``False`` forces the fingerprint."""
         if q.dtype not in _DTYPES or k_cache.dtype != q.dtype or v_cache.dtype != q.dtype:
             raise ShapeMismatch("q, k_cache, v_cache must share dtype float16 or bfloat16")
         if q.dim() != 3 or q.shape[1] != self.num_heads or q.shape[2] != self.head_dim:
@@ -220,7 +223,9 @@ class PatDeviceDecoder:
         self._captured = getattr(self, "_captured", False) or capturing
         ident = (block_tables.data_ptr(), block_tables._version, tuple(block_tables.shape), block_tables.stride(0),
                  seq_lens.data_ptr(), seq_lens._version)
-        flags = N.PAT_DECODE_SAME_TABLE if (ident == self._last_table and (capturing or not self._captured)) else 0
+        if same_table is None:
+            same_table = ident == self._last_table and (capturing or not self._captured)
+        flags = N.PAT_DECODE_SAME_TABLE if same_table else 0
         N.check(N.lib().pat_decoder_forward(
             self._h, C.c_void_p(block_tables.data_ptr()), block_tables.stride(0), C.c_void_p(seq_lens.data_ptr()),
             q.shape[0], block_tables.shape[1], C.c_void_p(q.data_ptr()), C.c_void_p(k_cache.data_ptr()),

@@ -1126,7 +1126,16 @@ __device__ void ph_hash(const int32_t* __restrict__ bt, int64_t stride, const in
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0 && acc) atomicAdd(acc_out, (unsigned long long)acc);
+  // one atomic per CTA, not per warp
+  __shared__ unsigned long long wacc[32];
+  if (lane == 0) wacc[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint64_t a = threadIdx.x < (blockDim.x >> 5) ? wacc[threadIdx.x] : 0;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    if (threadIdx.x == 0 && a) atomicAdd(acc_out, (unsigned long long)a);
+  }
 }
 
 #ifdef PAT_TC_TRACE
@@ -1151,6 +1160,7 @@ struct PlanState {
   int32_t* run;
   int32_t* nrun;
   unsigned* bar;  // [2] grid barrier
+  int32_t* fwd_sched;  // [4] the forward's claim counters, zeroed here
 };
 
 // The whole planner in ONE launch: fingerprint -> compare -> (only when the
@@ -1158,21 +1168,37 @@ struct PlanState {
 // DFS rank, nodes, pack order and members, then the schedule on CTA 0.
 __global__ void __launch_bounds__(1024, 1) k_plan(Ws w, Sched S, PlanState ps, int N2, int dyn_bytes) {
   extern __shared__ __align__(16) uint8_t dsm[];
+  if (blockIdx.x == 0 && threadIdx.x < 4) ps.fwd_sched[threadIdx.x] = 0;
   ph_hash(w.bt, w.stride, w.seq, w.B, w.bs, ps.h_acc);
-  grid_sync(ps.bar);
-  PLAN_STAMP(0);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const unsigned long long h = *ps.h_acc +
-        (((unsigned long long)(unsigned)w.B << 32) ^ (unsigned long long)(unsigned)w.bs ^ 0x7A7A000000000000ull);
-    *ps.h_acc = 0;
-    const bool changed = h != *ps.h_old;
-    *ps.run = changed ? 1 : 0;
-    if (changed) {
-      *ps.h_old = h;
-      atomicAdd(ps.nrun, 1);
+  // one barrier for fingerprint + compare: the last CTA to arrive compares
+  // the fingerprint and publishes the decision before releasing the others
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* bar = ps.bar;
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1) == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long h = *(volatile unsigned long long*)ps.h_acc +
+          (((unsigned long long)(unsigned)w.B << 32) ^ (unsigned long long)(unsigned)w.bs ^ 0x7A7A000000000000ull);
+      *ps.h_acc = 0;
+      const bool changed = h != *ps.h_old;
+      *ps.run = changed ? 1 : 0;
+      if (changed) {
+        *ps.h_old = h;
+        atomicAdd(ps.nrun, 1);
+      }
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1);
+    } else {
+      while (*gen == g) __nanosleep(64);
     }
+    __threadfence();
   }
-  grid_sync(ps.bar);
+  __syncthreads();
+  PLAN_STAMP(0);
   PLAN_STAMP(1);
   if (!*(volatile int32_t*)ps.run) return;
   {
@@ -1457,15 +1483,20 @@ int pat_decoder_forward(pat_decoder* Dc, const int32_t* block_tables, int64_t bt
   dev::Sched S = Dc->S;
   S.w = w;
   const int N2 = 2 * B + 2;
+  float* po = (float*)workspace;
+  const size_t so = ((size_t)Dc->S.cap_slots * Dc->H * Dc->d * 4 + 255) & ~size_t(255);
+  float* pl = (float*)((uint8_t*)workspace + so);
+  int32_t* sched = (int32_t*)((uint8_t*)workspace + pat_decoder_workspace_bytes(Dc) - 256);
   if (!(flags & PAT_DECODE_SAME_TABLE)) {
     // fingerprint, compare, and (only when the table changed) GPU packer +
-    // device schedule: ONE cooperative launch (grid barriers between phases)
+    // device schedule: ONE cooperative launch (grid barriers between phases);
+    // it also zeroes the forward's claim counters
     int P = 1;
     while (P < std::max(B, max_blocks)) P <<= 1;
     int PB = 1;
     while (PB < B) PB <<= 1;
     const int dyn = plan_smem(P, PB, 2 * Dc->Bmax + 2);
-    dev::PlanState ps{Dc->h_new, Dc->h_old, Dc->run, Dc->nrun, Dc->bar};
+    dev::PlanState ps{Dc->h_new, Dc->h_old, Dc->run, Dc->nrun, Dc->bar, sched};
     int n2 = N2, dynb = dyn;
     void* args[] = {(void*)&w, (void*)&S, (void*)&ps, (void*)&n2, (void*)&dynb};
     cudaError_t le = cudaLaunchCooperativeKernel((const void*)dev::k_plan, dim3(Dc->plan_grid), dim3(1024), args,
@@ -1474,16 +1505,11 @@ int pat_decoder_forward(pat_decoder* Dc, const int32_t* block_tables, int64_t bt
       set_error("pat_decoder_forward: planner launch: %s", cudaGetErrorString(le));
       return PAT_ERR_CUDA;
     }
-  }
-  // 4. forward + merge over the device plan (counts read on the device)
-  float* po = (float*)workspace;
-  const size_t so = ((size_t)Dc->S.cap_slots * Dc->H * Dc->d * 4 + 255) & ~size_t(255);
-  float* pl = (float*)((uint8_t*)workspace + so);
-  int32_t* sched = (int32_t*)((uint8_t*)workspace + pat_decoder_workspace_bytes(Dc) - 256);
-  if (cudaMemsetAsync(sched, 0, 16, st) != cudaSuccess) {
+  } else if (cudaMemsetAsync(sched, 0, 16, st) != cudaSuccess) {
     set_error("pat_decoder_forward: counter reset failed");
     return PAT_ERR_CUDA;
   }
+  // forward + merge over the device plan (counts read on the device)
   if (scale <= 0.f) scale = 1.0f / sqrtf((float)Dc->d);
   const float scale_log2 = scale * 1.4426950408889634f;
   cudaError_t e = launch_forward_tc(tmk, tmv, Dc->plan, VAR_TC, Dc->num_sms, dtype, Dc->d, q, out, po, pl, scale_log2,

@@ -54,6 +54,13 @@ def main(names):
             dec.forward(bt, sl, q, kc, vc, out=out, stream=s)
         torch.cuda.current_stream().wait_stream(s)
         t_same = timed(lambda i: gr.replay(), flush)
+        # the next layers of a step pass the same table tensors and skip even
+        # the fingerprint (PAT_DECODE_SAME_TABLE)
+        gr2 = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s), torch.cuda.graph(gr2, stream=s):
+            dec.forward(bt, sl, q, kc, vc, out=out, stream=s, same_table=True)
+        torch.cuda.current_stream().wait_stream(s)
+        t_next = timed(lambda i: gr2.replay(), flush)
         sl_alt = sl.clone()
         sl_alt[0] -= 1  # a different table: alternate between the two -> re-plan every replay
 
@@ -62,7 +69,7 @@ def main(names):
             gr.replay()
         t_replan = timed(flip, flush)
         print(f"{name}: host-planned layer {t_host:7.1f} us | device decoder: same table {t_same:7.1f} us, "
-              f"re-plan every step {t_replan:7.1f} us", flush=True)
+              f"re-plan every step {t_replan:7.1f} us, next layer (flag) {t_next:7.1f} us", flush=True)
         dec.close()
         plan.close()
 
