@@ -86,7 +86,8 @@ __device__ __forceinline__ long long gtime() {
   } while (0)
 #endif
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 448;  // per lane: producer, QK issuer, PV issuer; 2 x 4 softmax warps
+constexpr int kCtl = 6;        // control warps
 constexpr int kM = 128;  // rows per item (TMEM lanes)
 constexpr int kN = 32;   // tokens per KV tile
 #ifndef PAT_TC4_STAGES
@@ -131,10 +132,15 @@ struct Layout {
 enum Bar : int {
   KV_FULL = 0,
   KV_EMPTY = KV_FULL + kStages,
-  S_FULL = KV_EMPTY + kStages,  // [b] QK done
-  P_FULL = S_FULL + 2,          // [b] P written over S (4 warps)
-  SP_FREE = P_FULL + 2,         // [b] the PV reading P[b] completed (O updated, S/P[b] free)
-  O_EMPTY = SP_FREE + 2,        // epilogue has read O (one arrival after the lane's named barrier)
+  // One S and one P buffer per lane (TMEM columns 0-31 and 32-63): the next QK
+  // only waits for the softmax to have LOADED S, the softmax only waits for
+  // the previous PV before it WRITES P, so QK(c+1), softmax(c) and PV(c-1)
+  // overlap without a QK -> softmax -> PV -> QK chain through a shared buffer.
+  S_FULL = KV_EMPTY + kStages,  // QK(c) done
+  S_FREE = S_FULL + 1,          // softmax(c) loaded S (4 warps): QK(c+1) may overwrite it
+  P_FULL = S_FREE + 1,          // softmax(c) wrote P (4 warps)
+  P_FREE = P_FULL + 1,          // PV(c) completed: O updated, P free
+  O_EMPTY = P_FREE + 1,         // epilogue has read O (one arrival after the lane's named barrier)
   QT_FULL = O_EMPTY + 1,        // the item's Q rows stored in TMEM (4 warps)
   ITEM_FULL = QT_FULL + 1,      // [slot] published by the producer (32 lanes)
   ITEM_EMPTY = ITEM_FULL + 2,   // [slot] released by the MMA warp and the 4 softmax warps
@@ -196,9 +202,13 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return r;
 }
 __device__ __forceinline__ float ex2_approx(float v) {
+#ifdef PAT_EXP_FAKE  // timing experiment only: no MUFU work (wrong results)
+  return fmaf(v, 0.001f, 0.5f);
+#else
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
   return r;
+#endif
 }
 __device__ __forceinline__ int lds_s32(uint32_t a) {
   int v;
@@ -240,12 +250,12 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int ab_fmt, int a
          ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 __device__ __forceinline__ uint16_t bits16(uint32_t packed_lo) { return (uint16_t)(packed_lo & 0xffffu); }
-// shared-memory descriptor of an MN-major operand 16 elements (32 B) wide,
-// SWIZZLE_32B (layout type 6): 8-row K groups 256 B apart (SBO)
-__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+// shared-memory descriptor of an MN-major operand, SWIZZLE_32B (layout type 6):
+// 16-element (32 B) atoms along N `lbo` bytes apart, 8-row K groups 256 B apart (SBO)
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr, uint32_t lbo = 256u) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((256u >> 4) & 0x3FFF) << 16;  // LBO (one atom along N: unused)
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;  // LBO: next 16 N-elements
   d |= (uint64_t)((256u >> 4) & 0x3FFF) << 32;  // SBO
   d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
   d |= (uint64_t)6 << 61;                        // SWIZZLE_32B
@@ -278,8 +288,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef PAT_TC_TRACE
   const bool traced = (int)blockIdx.x == g_trace_cta;
 #endif
-  // lane (pipeline) of this warp: control warps 0,1 -> 0 and 2,3 -> 1; softmax 4-7 -> 0, 8-11 -> 1
-  const int pl = warp < 4 ? (warp >> 1) : ((warp - 4) >> 2);
+  // lane (pipeline) of this warp: control warps 0-2 -> 0 and 3-5 -> 1 (role = warp % 3:
+  // producer, QK issuer, PV issuer); softmax 6-9 -> 0, 10-13 -> 1
+  const int pl = warp < kCtl ? warp / 3 : ((warp - kCtl) >> 2);
+  const int role = warp < kCtl ? warp % 3 : 3;
   auto barL = [&](int l, int i) { return sb + L::kOffBar + (uint32_t)((l * BARS_PER_LANE + i) * 8); };
   auto bar = [&](int i) { return barL(pl, i); };
   // stage s of lane l's KV ring: K at sK(l, s) + kb * kPlane, V likewise
@@ -305,16 +317,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(ib(KV_FULL + s), 1);
       mbar_init(ib(KV_EMPTY + s), 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(ib(S_FULL + b), 1);
-      mbar_init(ib(P_FULL + b), 4);
-      mbar_init(ib(SP_FREE + b), 1);
-    }
+    mbar_init(ib(S_FULL), 1);
+    mbar_init(ib(S_FREE), 4);
+    mbar_init(ib(P_FULL), 4);
+    mbar_init(ib(P_FREE), 1);
     mbar_init(ib(O_EMPTY), 1);
     mbar_init(ib(QT_FULL), 4);
     for (int i = 0; i < 2; ++i) {
       mbar_init(ib(ITEM_FULL + i), 32);
-      mbar_init(ib(ITEM_EMPTY + i), 1 + 4);
+      mbar_init(ib(ITEM_EMPTY + i), 2 + 4);
       mbar_init(ib(JOIN_FULL + i), 1);
       mbar_init(ib(JOIN_EMPTY + i), 1);
     }
@@ -328,8 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tg = tmem + (uint32_t)(pl * 256);  // this lane's TMEM columns
 
-  if (warp < 4) {
-    if ((warp & 1) == 0) {
+  if (warp < kCtl) {
+    if (role == 0) {
       // ------------------------------------------------------------ producer
       if (elect_one()) {
         tma_prefetch(&tmk);
@@ -466,17 +477,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-      // ------------------------------------------------------------ MMA issuer
-      // Per lane tile c (S/P buffer b = c & 1): QK(c) needs its KV stage(s) and
-      // PV(c-2) done (it read P[b], which QK(c) overwrites); QK runs one tile
-      // ahead of PV, so the softmax of tile c overlaps QK(c+1).  The stage of
-      // ring position g is g % kStages of the lane's own ring, or of lane 0's
-      // ring for a joined pair item.  (Issuing PV from the softmax warpgroup
-      // after a named barrier instead measured slower: c4 219 -> 246 us.)
+      // ------------------------------------------------------------ MMA issuers
+      // Two warps per lane: one issues the QK products, the other the PV
+      // products.  A single thread's tcgen05.mma stream completes one M = 128
+      // instruction per ~65 cycles whatever N (tools/tmem_bench.cu), so one
+      // issuer per lane capped a 32-token tile at 12 x 65 cycles; with QK and
+      // PV on separate issuers they overlap and the tensor pipe approaches its
+      // floor.  QK(c) needs its KV stage(s) and PV(c-2) done (it overwrites
+      // S/P[c & 1]); PV(c) needs the softmax's P(c) and releases the stage(s).
+      // The stage of ring position g is g % kStages of the lane's own ring, or
+      // of lane 0's ring for a joined pair item.
       constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
       constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
       constexpr uint32_t idesc_qkn = idesc_f16(kM, kNarrow, Fmt<T>::ab, 0, 0);  // S^T = K Q^T
       constexpr uint32_t idesc_pvn = idesc_f16(kM, kNarrow, Fmt<T>::ab, 1, 1);  // O^T = V^T P^T
+      // (hi and lo P^T as the two halves of one N = 32 operand, reading V^T once,
+      // measured slower: register spills in the narrow epilogue)
+      const bool is_qk = role == 1;
       uint32_t tcnt = 0, rpos = 0, qu = 0, ou = 0;
       for (uint32_t n = 0;; ++n) {
         mbar_wait(bar(ITEM_FULL + (n & 1)), (n >> 1) & 1);
@@ -488,96 +505,97 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(ITEM_EMPTY + (n & 1)));
         if (it < 0) break;
-        if (src == pl && base != rpos) {  // a stage the producer skipped to align a narrow item
-          const int s = (int)(rpos % kStages);
-          mbar_wait(bar(KV_FULL + s), (rpos / kStages) & 1);
-          if (elect_one()) mbar_arrive(bar(KV_EMPTY + s));
-          __syncwarp();
-          rpos = base;
-        }
         const int ntiles = narrow ? (ntok + kNN - 1) / kNN : (ntok + kN - 1) / kN;
-        auto qk = [&](int t, bool first) {
-          const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
-          const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
-          const int s = (int)(g % kStages);
-          if (pl == 0) TC_TRACE(1, 2, c);
-          mbar_wait(barL(src, KV_FULL + s), (g / kStages) & 1);
-          if (narrow && ntok - t * kNN > kN) mbar_wait(barL(src, KV_FULL + s + 1), ((g + 1) / kStages) & 1);
-          if (pl == 0) TC_TRACE(1, 3, c);
-          mbar_wait(bar(SP_FREE + b), ((c >> 1) & 1) ^ 1);
-          if (first) mbar_wait(bar(QT_FULL), qu++ & 1);
-          tc_fence_after();
-          if (pl == 0) TC_TRACE(1, 0, c);
-          if (elect_one()) {
-            if (narrow) {
+        if (is_qk) {
+          for (int t = 0; t < ntiles; ++t) {
+            const uint32_t c = tcnt + (uint32_t)t;
+            const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
+            const int s = (int)(g % kStages);
+            if (pl == 0) TC_TRACE(1, 2, c);
+            mbar_wait(barL(src, KV_FULL + s), (g / kStages) & 1);
+            if (narrow && ntok - t * kNN > kN) mbar_wait(barL(src, KV_FULL + s + 1), ((g + 1) / kStages) & 1);
+            if (pl == 0) TC_TRACE(1, 3, c);
+            mbar_wait(bar(S_FREE), (c & 1) ^ 1);
+            if (t == 0) mbar_wait(bar(QT_FULL), qu++ & 1);
+            tc_fence_after();
+            if (pl == 0) TC_TRACE(1, 0, c);
+            if (elect_one()) {
+              if (narrow) {
 #pragma unroll
-              for (int k = 0; k < D / 16; ++k) {
-                const int kb = k >> 2, kk = k & 3;
-                const uint64_t ad = umma_desc_sw128(sK(src, s) + (uint32_t)(kb * L::kPlane + kk * 32), 16, 1024);
-                const uint64_t bd = umma_desc_sw128(sQn + (uint32_t)(kb * kNarrow * 128 + kk * 32), 16, 1024);
-                umma_f16_ss(tg + 32u * b, ad, bd, idesc_qkn, k > 0 ? 1u : 0u);
+                for (int k = 0; k < D / 16; ++k) {
+                  const int kb = k >> 2, kk = k & 3;
+                  const uint64_t ad = umma_desc_sw128(sK(src, s) + (uint32_t)(kb * L::kPlane + kk * 32), 16, 1024);
+                  const uint64_t bd = umma_desc_sw128(sQn + (uint32_t)(kb * kNarrow * 128 + kk * 32), 16, 1024);
+                  umma_f16_ss(tg, ad, bd, idesc_qkn, k > 0 ? 1u : 0u);
+                }
+              } else {
+                const uint64_t k0 = umma_desc_sw128(sK(src, s), 16, 1024);
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                  const int kb = k >> 2, kk = k & 3;
+                  // Q(m, k) packed two per column: a k-step of 16 = 8 columns
+                  umma_f16_ts(tg, tg + 64u + (uint32_t)(k * 8),
+                              k0 + (uint64_t)((kb * L::kPlane + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
+                }
               }
-            } else {
-              const uint64_t k0 = umma_desc_sw128(sK(src, s), 16, 1024);
+              umma_commit(bar(S_FULL));
+            }
+            __syncwarp();
+          }
+        } else {
+          if (src == pl && base != rpos) {  // a stage the producer skipped to align a narrow item
+            const int s = (int)(rpos % kStages);
+            mbar_wait(bar(KV_FULL + s), (rpos / kStages) & 1);
+            if (elect_one()) mbar_arrive(bar(KV_EMPTY + s));
+            __syncwarp();
+            rpos = base;
+          }
+          for (int t = 0; t < ntiles; ++t) {
+            const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
+            const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
+            const int s = (int)(g % kStages);
+            if (pl == 0) TC_TRACE(1, 4, c);
+            mbar_wait(bar(P_FULL), c & 1);
+            if (t == 0) mbar_wait(bar(O_EMPTY), (ou & 1) ^ 1);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t rel = src != pl ? barL(0, XKV_EMPTY + s) : bar(KV_EMPTY + s);
+              if (narrow) {
+                const int vt = min(kNN, ntok - t * kNN);
+                const int nk = (vt + 15) / 16;
+                for (int j = 0; j < nk; ++j) {
+                  const uint64_t ad = umma_desc_sw128(sV(src, s) + (uint32_t)(j * 16 * 128), L::kPlane, 1024);
+                  umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 0) + (uint32_t)(j * 512)), idesc_pvn,
+                              (t == 0 && j == 0) ? 0u : 1u);
+                  if constexpr (kSplit)
+                    umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 1) + (uint32_t)(j * 512)), idesc_pvn, 1u);
+                }
+                umma_commit(bar(P_FREE));
+                umma_commit(rel);
+                if (vt > kN) umma_commit(bar(KV_EMPTY + s + 1));
+              } else {
+                const uint64_t v0 = umma_desc_sw128(sV(src, s), L::kPlane, 1024);
 #pragma unroll
-              for (int k = 0; k < D / 16; ++k) {
-                const int kb = k >> 2, kk = k & 3;
-                // Q(m, k) packed two per column: a k-step of 16 = 8 columns
-                umma_f16_ts(tg + 32u * b, tg + 64u + (uint32_t)(k * 8),
-                            k0 + (uint64_t)((kb * L::kPlane + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
+                for (int k = 0; k < kN / 16; ++k) {
+                  const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
+                  // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
+                  umma_f16_ts(tg + 128u, tg + 32u + (uint32_t)(k * 8), bd, idesc_pv, (t == 0 && k == 0) ? 0u : 1u);
+                  if constexpr (kSplit)
+                    umma_f16_ts(tg + 128u, tg + 48u + (uint32_t)(k * 8), bd, idesc_pv, 1u);
+                }
+                umma_commit(bar(P_FREE));
+                umma_commit(rel);
               }
             }
-            umma_commit(bar(S_FULL + b));
+            __syncwarp();
+            if (pl == 0) TC_TRACE(1, 1, c);
           }
-          __syncwarp();
-        };
-        qk(0, true);
-        for (int t = 0; t < ntiles; ++t) {
-          const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
-          const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
-          const int s = (int)(g % kStages);
-          if (t + 1 < ntiles) qk(t + 1, false);
-          if (pl == 0) TC_TRACE(1, 4, c);
-          mbar_wait(bar(P_FULL + b), (c >> 1) & 1);
-          if (t == 0) mbar_wait(bar(O_EMPTY), (ou & 1) ^ 1);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t rel = src != pl ? barL(0, XKV_EMPTY + s) : bar(KV_EMPTY + s);
-            if (narrow) {
-              const int vt = min(kNN, ntok - t * kNN);
-              const int nk = (vt + 15) / 16;
-              for (int j = 0; j < nk; ++j) {
-                const uint64_t ad = umma_desc_sw128(sV(src, s) + (uint32_t)(j * 16 * 128), L::kPlane, 1024);
-                umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 0) + (uint32_t)(j * 512)), idesc_pvn,
-                            (t == 0 && j == 0) ? 0u : 1u);
-                if constexpr (kSplit)
-                  umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 1) + (uint32_t)(j * 512)), idesc_pvn,
-                              1u);
-              }
-              umma_commit(bar(SP_FREE + b));
-              umma_commit(rel);
-              if (vt > kN) umma_commit(bar(KV_EMPTY + s + 1));
-            } else {
-              const uint64_t v0 = umma_desc_sw128(sV(src, s), L::kPlane, 1024);
-#pragma unroll
-              for (int k = 0; k < kN / 16; ++k) {
-                const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
-                // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
-                umma_f16_ts(tg + 128u, tg + 32u * b + (uint32_t)(k * 8), bd, idesc_pv, (t == 0 && k == 0) ? 0u : 1u);
-                if constexpr (kSplit)
-                  umma_f16_ts(tg + 128u, tg + 32u * b + 16u + (uint32_t)(k * 8), bd, idesc_pv, 1u);
-              }
-              umma_commit(bar(SP_FREE + b));
-              umma_commit(rel);
-            }
-          }
-          __syncwarp();
-          if (pl == 0) TC_TRACE(1, 1, c);
+          ++ou;
+          if (src == pl) rpos = base + (uint32_t)((ntok + kN - 1) / kN);
         }
-        ++ou;
         tcnt += (uint32_t)ntiles;
-        if (src == pl) rpos = base + (uint32_t)((ntok + kN - 1) / kN);
       }
+      (void)qu;
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
@@ -598,45 +616,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int head = fld(n, kFKvh) * G + (fld(n, kFRow0) + r) % G;
       return reinterpret_cast<const uint4*>(qg + ((int64_t)qid * H + head) * D);
     };
-    // Q of item n into registers (zeros past its rows): a regular item's row
-    // `ln` (D / 2 words), or CPT 16-byte chunks of a narrow item's 16-row tile
     // narrow (transposed) items: <= 16 rows, tiles from the lane's own ring
     auto is_narrow = [&](uint32_t n) { return fld(n, kFNrows) <= kNarrow && !fld(n, kFShared); };
-    auto load_q = [&](uint32_t n, uint32_t* qv) {
+    auto prefetch_q_l1 = [&](uint32_t n) {
+      const int nr = fld(n, kFNrows);
+      if (is_narrow(n)) {
+        const int r = ln >> 3;
+        if (r < nr && (ln & 7) == 0) {
+          const char* a = reinterpret_cast<const char*>(q_row(n, r));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+          if (D * 2 > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 128));
+        }
+      } else if (ln < nr) {
+        const char* a = reinterpret_cast<const char*>(q_row(n, ln));
+#pragma unroll
+        for (int i = 0; i < D * 2 / 128; ++i) asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 128 * i));
+      }
+    };
+    // Q of item n (zeros past its rows) into TMEM -- a regular item's row `ln`,
+    // the A operand of QK, 32 columns at a time -- or into shared memory -- CPT
+    // 16-byte chunks of a narrow item's 16-row tile, the 128B-swizzled K-major
+    // B operand of S^T = K Q^T
+    auto put_q = [&](uint32_t n) {
       const int nr = fld(n, kFNrows);
       if (is_narrow(n)) {
         const int r = ln >> 3;
         const uint4* src = r < nr ? q_row(n, r) : nullptr;
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
-          const uint4 v = src ? __ldg(src + (ln & 7) * CPT + i) : make_uint4(0, 0, 0, 0);
-          qv[4 * i] = v.x, qv[4 * i + 1] = v.y, qv[4 * i + 2] = v.z, qv[4 * i + 3] = v.w;
-        }
-      } else {
-        const uint4* src = ln < nr ? q_row(n, ln) : nullptr;
-#pragma unroll
-        for (int i = 0; i < D / 8; ++i) {
-          const uint4 v = src ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
-          qv[4 * i] = v.x, qv[4 * i + 1] = v.y, qv[4 * i + 2] = v.z, qv[4 * i + 3] = v.w;
-        }
-      }
-    };
-    // ... then into TMEM (regular: the A operand of QK) or shared memory (narrow:
-    // the 128B-swizzled K-major B operand of S^T = K Q^T)
-    auto store_q = [&](uint32_t n, const uint32_t* qv) {
-      const int nr = fld(n, kFNrows);
-      if (is_narrow(n)) {
-        const int r = ln >> 3;
-#pragma unroll
-        for (int i = 0; i < CPT; ++i) {
           const int ch = (ln & 7) * CPT + i, kb = ch >> 3, cc = ch & 7;
-          st_shared_v4(sQn + (uint32_t)(kb * kNarrow * 128 + r * 128 + ((cc ^ (r & 7)) << 4)),
-                       make_uint4(qv[4 * i], qv[4 * i + 1], qv[4 * i + 2], qv[4 * i + 3]));
+          const uint4 v = src ? __ldg(src + ch) : make_uint4(0, 0, 0, 0);
+          st_shared_v4(sQn + (uint32_t)(kb * kNarrow * 128 + r * 128 + ((cc ^ (r & 7)) << 4)), v);
         }
         fence_proxy_async_smem();
       } else if (wq * 32 < nr) {
+        const uint4* src = ln < nr ? q_row(n, ln) : nullptr;
 #pragma unroll
-        for (int i = 0; i < D / 64; ++i) tmem_st32_nowait(sp + 64u + 32u * i, qv + 32 * i);
+        for (int i = 0; i < D / 64; ++i) {
+          uint32_t qv[32];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 v = src ? __ldg(src + 8 * i + j) : make_uint4(0, 0, 0, 0);
+            qv[4 * j] = v.x, qv[4 * j + 1] = v.y, qv[4 * j + 2] = v.z, qv[4 * j + 3] = v.w;
+          }
+          tmem_st32_nowait(sp + 64u + 32u * i, qv);
+        }
         tmem_wait_st();
       }
       tc_fence_before();
@@ -657,11 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
 
     wait_item(0);
-    if (fld(0, kFIdx) >= 0) {
-      uint32_t qv[D / 2];
-      load_q(0, qv);
-      store_q(0, qv);
-    }
+    if (fld(0, kFIdx) >= 0) put_q(0);
     for (uint32_t n = 0;; ++n) {
       if (fld(n, kFIdx) < 0) break;  // ITEM_FULL(n) already waited
       const int ntok = fld(n, kFNtok);
@@ -673,18 +693,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ntiles = narrow ? (ntok + kNN - 1) / kNN : (ntok + kN - 1) / kN;
       const uint32_t meta_s = ring_s + (n & 1) * kSlotBytes + kFMeta;
       bool have_next = false;
-      uint32_t qv[D / 2];
       long long it0 = 0, it1 = 0, it2 = 0, it3 = 0, it4 = 0, it5 = 0, it6 = 0;
       (void)it0, (void)it1, (void)it2, (void)it3, (void)it4, (void)it5, (void)it6;
 #ifdef PAT_TC_TRACE
       if (tr) ITEM_T(it0);
 #endif
-      // next item: fetch its Q rows at the start of this item's last tile
-      // (L2-warm: the producer prefetched them at claim time)
+      // next item: pull its Q rows into L1 at the start of this item's last
+      // tile (L2-warm: the producer prefetched them at claim time); they are
+      // loaded into registers only once this item's last S is consumed (holding
+      // them across the tile would cost 64 registers)
       auto prefetch_next_q = [&]() {
         wait_item(n + 1);
         have_next = fld(n + 1, kFIdx) >= 0;
-        if (have_next) load_q(n + 1, qv);
+        if (have_next) prefetch_q_l1(n + 1);
       };
 
       if (!narrow) {
@@ -693,18 +714,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         float m_ref = -INFINITY;             // running max, log2 units
         float2 l2 = make_float2(0.f, 0.f);
         for (int t = 0; t < ntiles; ++t) {
-          const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
+          const uint32_t c = tcnt + (uint32_t)t;
           if (t == ntiles - 1) prefetch_next_q();
-          mbar_wait(bar(S_FULL + b), (c >> 1) & 1);
+          mbar_wait(bar(S_FULL), c & 1);
 #ifdef PAT_TC_TRACE
           if (tr && t == 0) ITEM_T(it1);
           if (tr && pl == 0) TC_TRACE(2, 0, c);
 #endif
           tc_fence_after();
-          const uint32_t spb = sp + 32u * b;
+          // S in registers (or a warp without live rows): the next QK may overwrite it
+          auto release_s = [&]() {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(S_FREE));
+          };
+          if (!wlive) release_s();
           if (wlive) {
             uint32_t sr[kN];
-            tmem_ld32(spb, sr);
+            tmem_ld32(sp, sr);
+            release_s();
             const int valid = ntok - t * kN;
             if (valid < kN) {
 #pragma unroll
@@ -727,8 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float alpha = m_new == -INFINITY ? 1.f : ex2_approx(m_ref - m_new);
               if (t > 0) {
                 // O must hold the previous tile's PV before it is rescaled
-                const uint32_t cp = c - 1;
-                mbar_wait(bar(SP_FREE + (cp & 1)), (cp >> 1) & 1);
+                mbar_wait(bar(P_FREE), (c & 1) ^ 1);
                 tc_fence_after();
 #pragma unroll 1
                 for (int q = 0; q < D / 16; ++q) {
@@ -766,14 +793,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
               }
             }
-            tmem_st_n<kN / 2>(spb, ph);
-            if constexpr (kSplit) tmem_st_n<kN / 2>(spb + 16u, plo);
+            // P is free once the previous tile's PV completed
+            mbar_wait(bar(P_FREE), (c & 1) ^ 1);
+            tc_fence_after();
+            tmem_st_n<kN / 2>(sp + 32u, ph);
+            if constexpr (kSplit) tmem_st_n<kN / 2>(sp + 48u, plo);
+          } else {
+            // a warp without rows still waits for PV(c - 1) before its P_FULL(c)
+            // arrival: P_FULL is one barrier, so an arrival for tile c + 1 must
+            // not land in tile c's phase
+            mbar_wait(bar(P_FREE), (c & 1) ^ 1);
           }
           if (t * kN + kN > ntok) zero_v_tail(src, (int)((base + (uint32_t)t) % kStages), ntok - t * kN);
           if (wlive) tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar(P_FULL + b));
+          if (lane == 0) mbar_arrive(bar(P_FULL));
 #ifdef PAT_TC_TRACE
           if (tr && pl == 0) TC_TRACE(2, 1, c);
 #endif
@@ -783,14 +818,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         // The item's last QK completed (its S was consumed above): the next
         // item's Q goes in now, so its first QK overlaps this epilogue.
-        if (have_next) store_q(n + 1, qv);
+        if (have_next) put_q(n + 1);
 #ifdef PAT_TC_TRACE
         if (tr) ITEM_T(it4);
 #endif
 
         // ---- epilogue: the last PV of the item done -> O / l of this row
         const uint32_t gl = tcnt + (uint32_t)ntiles - 1;
-        mbar_wait(bar(SP_FREE + (gl & 1)), (gl >> 1) & 1);
+        mbar_wait(bar(P_FREE), gl & 1);
 #ifdef PAT_TC_TRACE
         if (tr) ITEM_T(it5);
 #endif
@@ -845,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s0 = (int)((base + 2u * (uint32_t)t) % kStages);
           const int vt = min(kNN, ntok - t * kNN);  // valid tokens of the tile
           if (t == ntiles - 1) prefetch_next_q();
-          mbar_wait(bar(S_FULL + b), (c >> 1) & 1);
+          mbar_wait(bar(S_FULL), c & 1);
 #ifdef PAT_TC_TRACE
           if (tr && t == 0) ITEM_T(it1);
           if (tr && pl == 0) TC_TRACE(2, 0, c);
@@ -855,7 +890,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bool need = false;
           if (tw) {
             uint32_t sr[kNarrow];
-            tmem_ld16(sp + 32u * b, sr);
+            tmem_ld16(sp, sr);
             const bool tv = ln < vt;
 #pragma unroll
             for (int r = 0; r < kNarrow; ++r) {
@@ -863,6 +898,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               need |= x[r] > m_ref[r] + kRescaleThreshold;
             }
           }
+          tc_fence_before();  // S^T is in registers: the next QK may overwrite it
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(S_FREE));
           if (bar_red_or(nbar, 128, need)) {
             // a row's max grew (always on the first tile): exact tile maxima
             // through shared memory, O^T / sums rescaled
@@ -887,8 +925,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (t > 0) {
               // O^T must hold the previous tile's PV before it is rescaled
-              const uint32_t cp = c - 1;
-              mbar_wait(bar(SP_FREE + (cp & 1)), (cp >> 1) & 1);
+              mbar_wait(bar(P_FREE), (c & 1) ^ 1);
               tc_fence_after();
               uint32_t o[kNarrow];
               tmem_ld16(sp + 128u, o);
@@ -919,6 +956,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 lsum[r + 1] += hv.y;
               }
             }
+            mbar_wait(bar(P_FREE), (c & 1) ^ 1);  // the previous PV read its P^T
             const uint32_t sw = (uint32_t)((ln >> 2) & 1);  // 32B swizzle: 16-byte chunk ^= bit 7 of the address
             const uint32_t a0 = (uint32_t)(ln * 32) + (sw << 4), a1 = (uint32_t)(ln * 32) + ((sw ^ 1u) << 4);
             st_shared_v4(sPn(b, 0) + a0, make_uint4(ph[0], ph[1], ph[2], ph[3]));
@@ -927,12 +965,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               st_shared_v4(sPn(b, 1) + a0, make_uint4(pq[0], pq[1], pq[2], pq[3]));
               st_shared_v4(sPn(b, 1) + a1, make_uint4(pq[4], pq[5], pq[6], pq[7]));
             }
+          } else {
+            mbar_wait(bar(P_FREE), (c & 1) ^ 1);  // see the regular path: one P_FULL phase per tile
           }
           if (vt < kNN && (vt % kN) != 0) zero_v_tail(pl, s0, vt);
           fence_proxy_async_smem();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar(P_FULL + b));
+          if (lane == 0) mbar_arrive(bar(P_FULL));
 #ifdef PAT_TC_TRACE
           if (tr && pl == 0) TC_TRACE(2, 1, c);
 #endif
@@ -940,7 +980,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef PAT_TC_TRACE
         if (tr) ITEM_T(it2);
 #endif
-        if (have_next) store_q(n + 1, qv);
+        if (have_next) put_q(n + 1);
 #ifdef PAT_TC_TRACE
         if (tr) ITEM_T(it4);
 #endif
@@ -957,7 +997,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) sts_f32(xch + (uint32_t)((2 * kNarrow + wq * kNarrow + r) * 4), v);
           }
         }
-        mbar_wait(bar(SP_FREE + (gl & 1)), (gl >> 1) & 1);
+        mbar_wait(bar(P_FREE), gl & 1);
 #ifdef PAT_TC_TRACE
         if (tr) ITEM_T(it5);
 #endif
