@@ -1010,23 +1010,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tr) ITEM_T(it6);
 #endif
         if (wq == 0 && lane == 0) mbar_arrive(bar(O_EMPTY));
+        // per-row scalars in parallel (thread = row): 1 / sum into the (now free)
+        // maxima slots, the partial's log-sum-exp straight to global memory
+        if (ln < nrows) {
+          const float Ls = lds_f32(xch + (uint32_t)((2 * kNarrow + ln) * 4)) +
+                           lds_f32(xch + (uint32_t)((3 * kNarrow + ln) * 4));
+          sts_f32(xch + (uint32_t)(ln * 4), __frcp_rn(Ls));
+          const int2 meta = lds_v2(meta_s + 8 * ln);
+          if (meta.y >= 0) {
+            float mr = m_ref[0];  // m_ref[ln] without dynamic register indexing
+#pragma unroll
+            for (int r = 1; r < kNarrow; ++r) mr = ln == r ? m_ref[r] : mr;
+            part_lse[(int64_t)meta.y * H + kvh * G + (row0 + ln) % G] = mr + log2f(Ls);
+          }
+        }
+        named_bar_sync(nbar, 128);
         if (ln < D) {
+          // then thread = head-dim lane: every row's scalars loaded up front, one
+          // coalesced row store each
+          float inv[kNarrow];
+          int2 mt[kNarrow];
+#pragma unroll
+          for (int r = 0; r < kNarrow; ++r) {
+            inv[r] = lds_f32(xch + (uint32_t)(r * 4));
+            mt[r] = lds_v2(meta_s + 8 * r);
+          }
           int gh = row0 % G;  // GQA head of row r within the kv head's group
 #pragma unroll
           for (int r = 0; r < kNarrow; ++r) {
             if (r >= nrows) break;
-            const float Ls = lds_f32(xch + (uint32_t)((2 * kNarrow + r) * 4)) +
-                             lds_f32(xch + (uint32_t)((3 * kNarrow + r) * 4));
-            const int2 meta = lds_v2(meta_s + 8 * r);
             const int head = kvh * G + gh;
             gh = gh + 1 == G ? 0 : gh + 1;
-            const float v = __uint_as_float(o[r]) * __frcp_rn(Ls);
-            if (meta.y < 0) {
-              out[((int64_t)meta.x * H + head) * D + ln] = Fmt<T>::cvt(v);
-            } else {
-              part_o[((int64_t)meta.y * H + head) * D + ln] = v;
-              if (ln == 0) part_lse[(int64_t)meta.y * H + head] = m_ref[r] + log2f(Ls);
-            }
+            const float v = __uint_as_float(o[r]) * inv[r];
+            if (mt[r].y < 0)
+              out[((int64_t)mt[r].x * H + head) * D + ln] = Fmt<T>::cvt(v);
+            else
+              part_o[((int64_t)mt[r].y * H + head) * D + ln] = v;
           }
         }
       }
