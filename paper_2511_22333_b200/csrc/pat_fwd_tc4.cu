@@ -490,9 +490,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_qk = umma_idesc_f16(kM, kN, Fmt<T>::ab, 0);
       constexpr uint32_t idesc_pv = umma_idesc_f16(kM, D, Fmt<T>::ab, 1);
       constexpr uint32_t idesc_qkn = idesc_f16(kM, kNarrow, Fmt<T>::ab, 0, 0);  // S^T = K Q^T
-      constexpr uint32_t idesc_pvn = idesc_f16(kM, kNarrow, Fmt<T>::ab, 1, 1);  // O^T = V^T P^T
-      // (hi and lo P^T as the two halves of one N = 32 operand, reading V^T once,
-      // measured slower: register spills in the narrow epilogue)
+      // O^T = V^T P^T; for bf16 the hi and lo P^T tiles (2 KB apart) are the two
+      // 16-column halves of ONE N = 32 operand: V^T is read once per k-step and
+      // O^T = [V^T P_hi^T | V^T P_lo^T] is summed in the epilogue
+      constexpr int kNO = kSplit ? 2 * kNarrow : kNarrow;
+      constexpr uint32_t idesc_pvn = idesc_f16(kM, kNO, Fmt<T>::ab, 1, 1);
       const bool is_qk = role == 1;
       uint32_t tcnt = 0, rpos = 0, qu = 0, ou = 0;
       for (uint32_t n = 0;; ++n) {
@@ -565,10 +567,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int nk = (vt + 15) / 16;
                 for (int j = 0; j < nk; ++j) {
                   const uint64_t ad = umma_desc_sw128(sV(src, s) + (uint32_t)(j * 16 * 128), L::kPlane, 1024);
-                  umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 0) + (uint32_t)(j * 512)), idesc_pvn,
+                  umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 0) + (uint32_t)(j * 512), kNarrow * 128), idesc_pvn,
                               (t == 0 && j == 0) ? 0u : 1u);
-                  if constexpr (kSplit)
-                    umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 1) + (uint32_t)(j * 512)), idesc_pvn, 1u);
                 }
                 umma_commit(bar(P_FREE));
                 umma_commit(rel);
@@ -927,11 +927,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               // O^T must hold the previous tile's PV before it is rescaled
               mbar_wait(bar(P_FREE), (c & 1) ^ 1);
               tc_fence_after();
-              uint32_t o[kNarrow];
-              tmem_ld16(sp + 128u, o);
+#pragma unroll 1
+              for (int h = 0; h < (kSplit ? 2 : 1); ++h) {  // the hi and lo halves of O^T
+                uint32_t o[kNarrow];
+                tmem_ld16(sp + 128u + (uint32_t)(h * kNarrow), o);
 #pragma unroll
-              for (int r = 0; r < kNarrow; ++r) o[r] = __float_as_uint(__uint_as_float(o[r]) * alpha[r]);
-              tmem_st16_wait(sp + 128u, o);
+                for (int r = 0; r < kNarrow; ++r) o[r] = __float_as_uint(__uint_as_float(o[r]) * alpha[r]);
+                tmem_st16_wait(sp + 128u + (uint32_t)(h * kNarrow), o);
+              }
             }
             named_bar_sync(nbar, 128);  // exchange slots read before they are reused
           }
@@ -1004,6 +1007,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         uint32_t o[kNarrow];
         tmem_ld16(sp + 128u, o);
+        if constexpr (kSplit) {
+          uint32_t o2[kNarrow];
+          tmem_ld16(sp + 128u + kNarrow, o2);
+#pragma unroll
+          for (int r = 0; r < kNarrow; ++r) o[r] = __float_as_uint(__uint_as_float(o[r]) + __uint_as_float(o2[r]));
+        }
         tc_fence_before();
         named_bar_sync(nbar, 128);  // sums published, O^T read by all four warps
 #ifdef PAT_TC_TRACE
