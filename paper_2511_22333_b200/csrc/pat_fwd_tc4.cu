@@ -618,21 +618,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     // narrow (transposed) items: <= 16 rows, tiles from the lane's own ring
     auto is_narrow = [&](uint32_t n) { return fld(n, kFNrows) <= kNarrow && !fld(n, kFShared); };
-    auto prefetch_q_l1 = [&](uint32_t n) {
-      const int nr = fld(n, kFNrows);
-      if (is_narrow(n)) {
-        const int r = ln >> 3;
-        if (r < nr && (ln & 7) == 0) {
-          const char* a = reinterpret_cast<const char*>(q_row(n, r));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
-          if (D * 2 > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 128));
-        }
-      } else if (ln < nr) {
-        const char* a = reinterpret_cast<const char*>(q_row(n, ln));
-#pragma unroll
-        for (int i = 0; i < D * 2 / 128; ++i) asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 128 * i));
-      }
-    };
     // Q of item n (zeros past its rows) into TMEM -- a regular item's row `ln`,
     // the A operand of QK, 32 columns at a time -- or into shared memory -- CPT
     // 16-byte chunks of a narrow item's 16-row tile, the 128B-swizzled K-major
@@ -698,14 +683,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef PAT_TC_TRACE
       if (tr) ITEM_T(it0);
 #endif
-      // next item: pull its Q rows into L1 at the start of this item's last
-      // tile (L2-warm: the producer prefetched them at claim time); they are
-      // loaded into registers only once this item's last S is consumed (holding
-      // them across the tile would cost 64 registers)
+      // next item: known at the start of this item's last tile; its Q rows
+      // (L2-warm: the producer prefetched them at claim time) are loaded once
+      // this item's last S is consumed.  (Holding them in registers across the
+      // tile cost 64 registers; an L1 prefetch stalled the softmax warps: c4
+      // 201 -> 197 us without it.)
       auto prefetch_next_q = [&]() {
         wait_item(n + 1);
         have_next = fld(n + 1, kFIdx) >= 0;
-        if (have_next) prefetch_q_l1(n + 1);
+
       };
 
       if (!narrow) {
