@@ -559,8 +559,7 @@ def main():
                          "traffic": traffic["bytes"] if traffic else None,
                          "layer_traffic": traffic["layer_bytes"] if traffic else None,
                          "traffic_source": traffic["source"] if traffic else None,
-                         "kernel": "dominant kernel = the forward (tcgen05 fwd_tc4_kernel; fwd_stream_kernel for "
-                                   "all-narrow plans), timed live with CUDA events as a graph of the same plan without "
+                         "kernel": "dominant kernel = the forward (tcgen05 fwd_tc4_kernel), timed live with CUDA events as a graph of the same plan without "
                                    "the merge launch; achieved = unique KV bytes / its time; layer_* = forward + "
                                    "merge_kernel; traffic = DRAM read+write of the forward kernel per launch, layer_traffic "
                                    "of all the layer's kernels (ncu)",

@@ -224,17 +224,11 @@ int upload(pat_plan* P) {
 }
 
 int finish_plan(pat_plan* P, const RowsView& R, int flags) {
-  if (P->tc_auto) {
-    // Kernel choice: every pack goes to the tcgen05 kernel (one persistent
-    // kernel, dynamic load balance), except when no pack is wider than one
-    // 16-row mma.sync tile (e.g. a batch without prefix sharing): then the
-    // HBM-paced streaming kernel alone is faster (measured: c5 694 vs 800 us).
-    int max_rows = 0;
-    const int G = P->H / P->KVH;
-    for (int p = 0; p < P->packs.n_packs(); ++p)
-      max_rows = std::max(max_rows, (P->packs.q_off[p + 1] - P->packs.q_off[p]) * G);
-    P->tc_min_rows = max_rows <= 16 ? 0 : 1;
-  }
+  // Kernel choice (options value 0): every pack goes to the tcgen05 kernel --
+  // one persistent kernel with dynamic load balance, narrow packs transposed.
+  // (Round 1 kept the mma.sync streaming kernel for plans without a pack wider
+  // than 16 rows; the round-2 narrow path is faster there too: c5 622 vs 688 us.)
+  if (P->tc_auto) P->tc_min_rows = 1;
   ScheduleParams sp{P->B, P->bs, P->H, P->KVH, P->d, P->split_mode, P->num_sms, P->tc_min_rows};
   sp.pair_items = (flags & PAT_PLAN_PAIR_ITEMS) != 0;
   sp.all_partials = (flags & PAT_PLAN_ALL_PARTIALS) != 0;
