@@ -506,6 +506,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 template <int D, typename T>
 __global__ void __launch_bounds__(256) merge_kernel(DevPlan plan, const float* __restrict__ part_o,
                                                     const float* __restrict__ part_lse, T* __restrict__ out) {
+  // launched as a programmatic dependent of the forward (launch_merge): the
+  // CTAs are resident when the forward drains; wait for its partials here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   PAT_SPAN_BEGIN(g_span_mma, 1);
   merge_rows<D, T>(plan, part_o, part_lse, out, (blockIdx.x * blockDim.x + threadIdx.x) >> 5,
                    (gridDim.x * blockDim.x) >> 5);
@@ -560,17 +563,32 @@ cudaError_t launch_forward_variant(const CUtensorMap& tmk, const CUtensorMap& tm
   return launch_fwd_d<64, __nv_bfloat16>(tmk, tmv, plan, var, grid, q, out, po, pl, scale_log2, st);
 }
 
-cudaError_t launch_merge(const DevPlan& plan, int grid, int dtype, int d, const float* po, const float* pl,
-                         void* out, cudaStream_t st) {
-  if (dtype == PAT_DTYPE_F16) {
-    if (d == 128) merge_kernel<128, __half><<<grid, 256, 0, st>>>(plan, po, pl, (__half*)out);
-    else merge_kernel<64, __half><<<grid, 256, 0, st>>>(plan, po, pl, (__half*)out);
-  } else {
-    if (d == 128) merge_kernel<128, __nv_bfloat16><<<grid, 256, 0, st>>>(plan, po, pl, (__nv_bfloat16*)out);
-    else merge_kernel<64, __nv_bfloat16><<<grid, 256, 0, st>>>(plan, po, pl, (__nv_bfloat16*)out);
-  }
-  return cudaGetLastError();
+template <int D, typename T>
+static cudaError_t launch_merge_t(const DevPlan& plan, int grid, const float* po, const float* pl, void* out,
+                                  cudaStream_t st) {
+  // programmatic dependent launch: the merge grid is scheduled while the
+  // forward drains (its CTAs block in griddepcontrol.wait until the forward
+  // grid completed and flushed), hiding the launch gap between the two kernels
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, merge_kernel<D, T>, plan, po, pl, (T*)out);
 }
 
+cudaError_t launch_merge(const DevPlan& plan, int grid, int dtype, int d, const float* po, const float* pl,
+                         void* out, cudaStream_t st) {
+  if (dtype == PAT_DTYPE_F16)
+    return d == 128 ? launch_merge_t<128, __half>(plan, grid, po, pl, out, st)
+                    : launch_merge_t<64, __half>(plan, grid, po, pl, out, st);
+  return d == 128 ? launch_merge_t<128, __nv_bfloat16>(plan, grid, po, pl, out, st)
+                  : launch_merge_t<64, __nv_bfloat16>(plan, grid, po, pl, out, st);
+}
 
 }  // namespace pat

@@ -338,6 +338,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tg = tmem + (uint32_t)(pl * 256);  // this lane's TMEM columns
+  // the merge kernel (a programmatic dependent) may be scheduled now: its CTAs
+  // take SMs as this grid's CTAs exit and wait for the whole grid there
+  asm volatile("griddepcontrol.launch_dependents;");
 
   if (warp < kCtl) {
     if (role == 0) {
