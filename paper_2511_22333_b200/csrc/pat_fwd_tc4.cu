@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #ifdef PAT_TC_TRACE
   const bool traced = (int)blockIdx.x == g_trace_cta;
+  if (tid == 0 && blockIdx.x < kSpanCtas) g_span_tc[0][blockIdx.x][0] = (unsigned long long)gtime();
 #endif
   // lane (pipeline) of this warp: control warps 0-2 -> 0 and 3-5 -> 1 (role = warp % 3:
   // producer, QK issuer, PV issuer); softmax 6-9 -> 0, 10-13 -> 1
@@ -1069,6 +1070,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
+#ifdef PAT_TC_TRACE
+  if (tid == 0 && blockIdx.x < kSpanCtas) g_span_tc[0][blockIdx.x][1] = (unsigned long long)gtime();
+#endif
   if (tid == 0) {
     // the last CTA out re-arms the item counter for the next launch
     __threadfence();

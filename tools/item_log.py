@@ -50,6 +50,9 @@ def run(name, tc_min_rows=0):
         P.pat_attention(plan, q, kc, vc, out=out, workspace=ws)
         torch.cuda.synchronize()
     lib.pat_debug_item_log(log.ctypes.data, cnt.ctypes.data)
+    spans = np.zeros((1, 4096, 2), dtype=np.uint64)
+    lib.pat_debug_spans_tc.argtypes = [C.c_void_p]
+    lib.pat_debug_spans_tc(spans.ctypes.data)
     n = int(cnt[0])
     e = log[:n]
     t0 = e[:, 4].min()
@@ -59,6 +62,11 @@ def run(name, tc_min_rows=0):
     tiles = (e[:, 6] - e[:, 5]) / 1e3
     epi = (e[:, 7] - e[:, 6]) / 1e3
     print(f"== {name}: {n} items, layer span {span:.1f} us (first item start -> last epilogue)")
+    sp = spans[0][spans[0][:, 0] > 0].astype(np.int64)
+    if len(sp):
+        print(f"   kernel: CTA entry (first / last) -> first item start {(t0 - sp[:, 0].min()) / 1e3:.1f} / "
+              f"{(t0 - sp[:, 0].max()) / 1e3:.1f} us;  last epilogue -> last CTA exit {(sp[:, 1].max() - end) / 1e3:.1f} us; "
+              f"entry spread {(sp[:, 0].max() - sp[:, 0].min()) / 1e3:.1f} us")
     ncta = int(e[:, 0].max()) + 1
     idle = np.zeros(ncta)
     first = np.zeros(ncta)
