@@ -41,6 +41,8 @@ struct Ws {
   int32_t* valid;
   int32_t* err;     // [0] status, [1] row
   int32_t* lcp;     // [B*B]
+  unsigned long long* hs;  // [B * hs_n] prefix hashes of each row's 32-position segments
+  int hs_n;                // segments per row (ceil(maxb / 32))
   int32_t* K;       // internal levels
   int32_t* hasleaf;
   int32_t* end;     // [B*D]
@@ -133,10 +135,50 @@ __global__ void k_rows(Ws w) {
   ph_rows(w);
 }
 
-// one CTA per row: bitonic sort of the row's block ids in smem, adjacent compare
+__device__ __forceinline__ uint64_t lcp_mix(uint64_t z) {  // splitmix64 finaliser
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// hash term of (position, block id, tokens) of a row
+__device__ __forceinline__ uint64_t lcp_term(const Ws& w, int q, int p) {
+  return lcp_mix(lcp_mix(((uint64_t)(uint32_t)p << 32) | (uint32_t)blk_at(w, q, p)) + (uint64_t)(uint32_t)tok_at(w, q, p));
+}
+
+// one CTA per row: the row's segment prefix hashes (for the LCP phase), then a
+// bitonic sort of its block ids in smem, adjacent compare
 __device__ void ph_dup(const Ws& w, int32_t* sbuf) {
   for (int q = blockIdx.x; q < w.B; q += gridDim.x) {
   const int n = min(w.nblk[q], w.maxb);
+  {
+    // hs[q][s] = sum of the terms of positions [0, 32 (s + 1)) (order-free sum
+    // of position-keyed terms: equal prefixes give equal values)
+    const int S = (n + 31) / 32, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned long long* seg = reinterpret_cast<unsigned long long*>(sbuf);
+    for (int sg = wid; sg < S; sg += nw) {
+      const int p = 32 * sg + lane;
+      uint64_t x = p < n ? lcp_term(w, q, p) : 0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) seg[sg] = x;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      uint64_t carry = 0;
+      for (int s0 = 0; s0 < S; s0 += 32) {
+        uint64_t x = s0 + lane < S ? seg[s0 + lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (s0 + lane < S) w.hs[(int64_t)q * w.hs_n + s0 + lane] = x + carry;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+    }
+    __syncthreads();
+  }
   if (n <= 1) continue;
   int P = 1;
   while (P < n) P <<= 1;
@@ -183,8 +225,24 @@ __device__ void ph_lcp(const Ws& w) {
       continue;
     }
     const int n = min(w.nblk[q], w.nblk[r]);
+    // coarse: the first 32-position segment whose prefix hashes differ (the
+    // segments before the last one lie inside both rows); then position by
+    // position from there (a hash difference the positions do not confirm
+    // cannot happen, but would only make the scan continue)
+    const int S = (n + 31) / 32;
+    int s_first = S > 0 ? S - 1 : 0;
+    const unsigned long long* hq = w.hs + (int64_t)q * w.hs_n;
+    const unsigned long long* hr = w.hs + (int64_t)r * w.hs_n;
+    for (int s0 = 0; s0 < S - 1; s0 += 32) {
+      const int sg = s0 + lane;
+      const unsigned m = __ballot_sync(0xffffffffu, sg < S - 1 && hq[sg] != hr[sg]);
+      if (m) {
+        s_first = s0 + __ffs(m) - 1;
+        break;
+      }
+    }
     int l = n;
-    for (int p0 = 0; p0 < n; p0 += 32) {
+    for (int p0 = 32 * s_first; p0 < n; p0 += 32) {
       const int p = p0 + lane;
       bool diff = false;
       if (p < n) diff = blk_at(w, q, p) != blk_at(w, r, p) || tok_at(w, q, p) != tok_at(w, r, p);
@@ -568,7 +626,9 @@ int device_pack(const int32_t* d_bt, int64_t stride, const int32_t* d_seq, int B
   w.maxb = maxb;
   w.D = D;
   const size_t BB = (size_t)B * B, BD = (size_t)B * D, BD1 = (size_t)B * D1, N2 = 2 * (size_t)B + 2;
-  fields = {{&w.nblk, (size_t)B}, {&w.valid, (size_t)B}, {&w.err, 2}, {&w.lcp, BB}, {&w.K, (size_t)B},
+  w.hs_n = (maxb + 31) / 32;
+  fields = {{&w.nblk, (size_t)B}, {&w.valid, (size_t)B}, {&w.err, 2}, {&w.lcp, BB},
+            {reinterpret_cast<int32_t**>(&w.hs), (size_t)B * w.hs_n * 2}, {&w.K, (size_t)B},
             {&w.hasleaf, (size_t)B}, {&w.end, BD}, {&w.nq, BD}, {&w.minq, BD}, {&w.term, BD},
             {&w.start, BD1}, {&w.stop, BD1}, {&w.span, BD1}, {&w.anchor, BD1}, {&w.member, BD1},
             {&w.nmemb, (size_t)B}, {&w.k0, (size_t)B}, {&w.cnt_own, (size_t)B}, {&w.pi, (size_t)B},
@@ -599,7 +659,7 @@ int device_pack(const int32_t* d_bt, int64_t stride, const int32_t* d_seq, int B
   dev::k_rows<<<gq, TB, 0, st>>>(w);
   int P = 1;
   while (P < std::max(B, maxb)) P <<= 1;
-  const int dup_smem = std::max(P, 1) * 4;
+  const int dup_smem = std::max(P * 4, 256);  // also the row's segment sums (8 B per 32 blocks)
   if (dup_smem > 48 * 1024) cudaFuncSetAttribute(dev::k_dup, cudaFuncAttributeMaxDynamicSharedMemorySize, dup_smem);
   dev::k_dup<<<B, 256, dup_smem, st>>>(w);
   {
@@ -1327,6 +1387,7 @@ int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t m
   dev::Sched& S = Dc->S;
   std::vector<F> f = {
       {(void**)&w.nblk, Bz * 4}, {(void**)&w.valid, Bz * 4}, {(void**)&w.err, 8}, {(void**)&w.lcp, BB * 4},
+      {(void**)&w.hs, Bz * ((max_blocks + 31) / 32) * 8},
       {(void**)&w.K, Bz * 4}, {(void**)&w.hasleaf, Bz * 4}, {(void**)&w.end, BD * 4}, {(void**)&w.nq, BD * 4},
       {(void**)&w.minq, BD * 4}, {(void**)&w.term, BD * 4}, {(void**)&w.start, BD1 * 4}, {(void**)&w.stop, BD1 * 4},
       {(void**)&w.span, BD1 * 4}, {(void**)&w.anchor, BD1 * 4}, {(void**)&w.member, BD1 * 4},
@@ -1382,6 +1443,7 @@ int pat_decoder_create(const pat_plan_options* opt, int32_t max_batch, int32_t m
   w.D = D;
   w.bs = block_size;
   w.run = Dc->run;
+  w.hs_n = (max_blocks + 31) / 32;
   S.cap_blk = (int)cap_blk;
   S.cap_units = (int)cap_units;
   S.cap_members = (int)cap_members;
