@@ -132,15 +132,16 @@ struct Layout {
 enum Bar : int {
   KV_FULL = 0,
   KV_EMPTY = KV_FULL + kStages,
-  // One S and one P buffer per lane (TMEM columns 0-31 and 32-63): the next QK
-  // only waits for the softmax to have LOADED S, the softmax only waits for
-  // the previous PV before it WRITES P, so QK(c+1), softmax(c) and PV(c-1)
-  // overlap without a QK -> softmax -> PV -> QK chain through a shared buffer.
-  S_FULL = KV_EMPTY + kStages,  // QK(c) done
-  S_FREE = S_FULL + 1,          // softmax(c) loaded S (4 warps): QK(c+1) may overwrite it
-  P_FULL = S_FREE + 1,          // softmax(c) wrote P (4 warps)
-  P_FREE = P_FULL + 1,          // PV(c) completed: O updated, P free
-  O_EMPTY = P_FREE + 1,         // epilogue has read O (one arrival after the lane's named barrier)
+  // Two S/P buffers per lane (TMEM columns 32b .. 32b + 31, b = tile & 1): the
+  // softmax writes P(c) over the S(c) it has loaded (hi at +0, lo at +16), so
+  // QK(c) waits only for PV(c-2) -- the last reader of its buffer -- and runs a
+  // whole tile ahead of the softmax, which never waits for a PV before writing
+  // P.  Every barrier of the chain is per buffer: an arrival for tile c + 2
+  // needs PV(c), so no arrival can land in another tile's phase.
+  S_FULL = KV_EMPTY + kStages,  // [b] QK(c) done
+  P_FULL = S_FULL + 2,          // [b] softmax(c) wrote P (4 warps)
+  P_FREE = P_FULL + 2,          // [b] PV(c) completed: O updated, buffer b free
+  O_EMPTY = P_FREE + 2,         // epilogue has read O (one arrival after the lane's named barrier)
   QT_FULL = O_EMPTY + 1,        // the item's Q rows stored in TMEM (4 warps)
   ITEM_FULL = QT_FULL + 1,      // [slot] published by the producer (32 lanes)
   ITEM_EMPTY = ITEM_FULL + 2,   // [slot] released by the MMA warp and the 4 softmax warps
@@ -318,10 +319,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(ib(KV_FULL + s), 1);
       mbar_init(ib(KV_EMPTY + s), 1);
     }
-    mbar_init(ib(S_FULL), 1);
-    mbar_init(ib(S_FREE), 4);
-    mbar_init(ib(P_FULL), 4);
-    mbar_init(ib(P_FREE), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(ib(S_FULL + b), 1);
+      mbar_init(ib(P_FULL + b), 4);
+      mbar_init(ib(P_FREE + b), 1);
+    }
     mbar_init(ib(O_EMPTY), 1);
     mbar_init(ib(QT_FULL), 4);
     for (int i = 0; i < 2; ++i) {
@@ -521,8 +523,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(barL(src, KV_FULL + s), (g / kStages) & 1);
             if (narrow && ntok - t * kNN > kN) mbar_wait(barL(src, KV_FULL + s + 1), ((g + 1) / kStages) & 1);
             if (pl == 0) TC_TRACE(1, 3, c);
-            mbar_wait(bar(S_FREE), (c & 1) ^ 1);
+            // buffer c & 1 was last read by PV(c - 2)
+            mbar_wait(bar(P_FREE + (c & 1)), ((c >> 1) & 1) ^ 1);
             if (t == 0) mbar_wait(bar(QT_FULL), qu++ & 1);
+            const uint32_t sbuf = tg + 32u * (c & 1);
             tc_fence_after();
             if (pl == 0) TC_TRACE(1, 0, c);
             if (elect_one()) {
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const int kb = k >> 2, kk = k & 3;
                   const uint64_t ad = umma_desc_sw128(sK(src, s) + (uint32_t)(kb * L::kPlane + kk * 32), 16, 1024);
                   const uint64_t bd = umma_desc_sw128(sQn + (uint32_t)(kb * kNarrow * 128 + kk * 32), 16, 1024);
-                  umma_f16_ss(tg, ad, bd, idesc_qkn, k > 0 ? 1u : 0u);
+                  umma_f16_ss(sbuf, ad, bd, idesc_qkn, k > 0 ? 1u : 0u);
                 }
               } else {
                 const uint64_t k0 = umma_desc_sw128(sK(src, s), 16, 1024);
@@ -540,11 +544,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < D / 16; ++k) {
                   const int kb = k >> 2, kk = k & 3;
                   // Q(m, k) packed two per column: a k-step of 16 = 8 columns
-                  umma_f16_ts(tg, tg + 64u + (uint32_t)(k * 8),
+                  umma_f16_ts(sbuf, tg + 64u + (uint32_t)(k * 8),
                               k0 + (uint64_t)((kb * L::kPlane + kk * 32) >> 4), idesc_qk, k > 0 ? 1u : 0u);
                 }
               }
-              umma_commit(bar(S_FULL));
+              umma_commit(bar(S_FULL + (c & 1)));
             }
             __syncwarp();
           }
@@ -561,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
             const int s = (int)(g % kStages);
             if (pl == 0) TC_TRACE(1, 4, c);
-            mbar_wait(bar(P_FULL), c & 1);
+            mbar_wait(bar(P_FULL + b), (c >> 1) & 1);
             if (t == 0) mbar_wait(bar(O_EMPTY), (ou & 1) ^ 1);
             tc_fence_after();
             if (elect_one()) {
@@ -574,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   umma_f16_ss(tg + 128u, ad, desc_sw32(sPn(b, 0) + (uint32_t)(j * 512), kNarrow * 128), idesc_pvn,
                               (t == 0 && j == 0) ? 0u : 1u);
                 }
-                umma_commit(bar(P_FREE));
+                umma_commit(bar(P_FREE + b));
                 umma_commit(rel);
                 if (vt > kN) umma_commit(bar(KV_EMPTY + s + 1));
               } else {
@@ -583,11 +587,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < kN / 16; ++k) {
                   const uint64_t bd = v0 + (uint64_t)((k * 16 * 128) >> 4);
                   // P(m, k) is packed two per column: a k-step of 16 tokens = 8 columns
-                  umma_f16_ts(tg + 128u, tg + 32u + (uint32_t)(k * 8), bd, idesc_pv, (t == 0 && k == 0) ? 0u : 1u);
+                  umma_f16_ts(tg + 128u, tg + 32u * b + (uint32_t)(k * 8), bd, idesc_pv, (t == 0 && k == 0) ? 0u : 1u);
                   if constexpr (kSplit)
-                    umma_f16_ts(tg + 128u, tg + 48u + (uint32_t)(k * 8), bd, idesc_pv, 1u);
+                    umma_f16_ts(tg + 128u, tg + 32u * b + 16u + (uint32_t)(k * 8), bd, idesc_pv, 1u);
                 }
-                umma_commit(bar(P_FREE));
+                umma_commit(bar(P_FREE + b));
                 umma_commit(rel);
               }
             }
@@ -705,24 +709,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2 l2 = make_float2(0.f, 0.f);
         for (int t = 0; t < ntiles; ++t) {
           const uint32_t c = tcnt + (uint32_t)t;
+          const uint32_t sb_c = sp + 32u * (c & 1);  // this tile's S/P buffer
           if (t == ntiles - 1) prefetch_next_q();
-          mbar_wait(bar(S_FULL), c & 1);
+          mbar_wait(bar(S_FULL + (c & 1)), (c >> 1) & 1);
 #ifdef PAT_TC_TRACE
           if (tr && t == 0) ITEM_T(it1);
           if (tr && pl == 0) TC_TRACE(2, 0, c);
 #endif
           tc_fence_after();
-          // S in registers (or a warp without live rows): the next QK may overwrite it
-          auto release_s = [&]() {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(S_FREE));
-          };
-          if (!wlive) release_s();
           if (wlive) {
             uint32_t sr[kN];
-            tmem_ld32(sp, sr);
-            release_s();
+            tmem_ld32(sb_c, sr);
             const int valid = ntok - t * kN;
             if (valid < kN) {
 #pragma unroll
@@ -745,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float alpha = m_new == -INFINITY ? 1.f : ex2_approx(m_ref - m_new);
               if (t > 0) {
                 // O must hold the previous tile's PV before it is rescaled
-                mbar_wait(bar(P_FREE), (c & 1) ^ 1);
+                mbar_wait(bar(P_FREE + ((c - 1) & 1)), ((c - 1) >> 1) & 1);
                 tc_fence_after();
 #pragma unroll 1
                 for (int q = 0; q < D / 16; ++q) {
@@ -783,22 +780,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l2 = __fadd2_rn(l2, Fmt<T>::unpack(ph[k]));
               }
             }
-            // P is free once the previous tile's PV completed
-            mbar_wait(bar(P_FREE), (c & 1) ^ 1);
-            tc_fence_after();
-            tmem_st_n<kN / 2>(sp + 32u, ph);
-            if constexpr (kSplit) tmem_st_n<kN / 2>(sp + 48u, plo);
-          } else {
-            // a warp without rows still waits for PV(c - 1) before its P_FULL(c)
-            // arrival: P_FULL is one barrier, so an arrival for tile c + 1 must
-            // not land in tile c's phase
-            mbar_wait(bar(P_FREE), (c & 1) ^ 1);
+            // P over this tile's S (already in registers: tmem_ld32 waited)
+            tmem_st_n<kN / 2>(sb_c, ph);
+            if constexpr (kSplit) tmem_st_n<kN / 2>(sb_c + 16u, plo);
           }
           if (t * kN + kN > ntok) zero_v_tail(src, (int)((base + (uint32_t)t) % kStages), ntok - t * kN);
           if (wlive) tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar(P_FULL));
+          if (lane == 0) mbar_arrive(bar(P_FULL + (c & 1)));
 #ifdef PAT_TC_TRACE
           if (tr && pl == 0) TC_TRACE(2, 1, c);
 #endif
@@ -815,7 +805,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         // ---- epilogue: the last PV of the item done -> O / l of this row
         const uint32_t gl = tcnt + (uint32_t)ntiles - 1;
-        mbar_wait(bar(P_FREE), gl & 1);
+        mbar_wait(bar(P_FREE + (gl & 1)), (gl >> 1) & 1);
 #ifdef PAT_TC_TRACE
         if (tr) ITEM_T(it5);
 #endif
@@ -870,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s0 = (int)((base + 2u * (uint32_t)t) % kStages);
           const int vt = min(kNN, ntok - t * kNN);  // valid tokens of the tile
           if (t == ntiles - 1) prefetch_next_q();
-          mbar_wait(bar(S_FULL), c & 1);
+          mbar_wait(bar(S_FULL + b), (c >> 1) & 1);
 #ifdef PAT_TC_TRACE
           if (tr && t == 0) ITEM_T(it1);
           if (tr && pl == 0) TC_TRACE(2, 0, c);
@@ -880,7 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bool need = false;
           if (tw) {
             uint32_t sr[kNarrow];
-            tmem_ld16(sp, sr);
+            tmem_ld16(sp + 32u * b, sr);
             const bool tv = ln < vt;
 #pragma unroll
             for (int r = 0; r < kNarrow; ++r) {
@@ -888,9 +878,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               need |= x[r] > m_ref[r] + kRescaleThreshold;
             }
           }
-          tc_fence_before();  // S^T is in registers: the next QK may overwrite it
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar(S_FREE));
           if (bar_red_or(nbar, 128, need)) {
             // a row's max grew (always on the first tile): exact tile maxima
             // through shared memory, O^T / sums rescaled
@@ -915,7 +902,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (t > 0) {
               // O^T must hold the previous tile's PV before it is rescaled
-              mbar_wait(bar(P_FREE), (c & 1) ^ 1);
+              mbar_wait(bar(P_FREE + (b ^ 1u)), ((c - 1) >> 1) & 1);
               tc_fence_after();
 #pragma unroll 1
               for (int h = 0; h < (kSplit ? 2 : 1); ++h) {  // the hi and lo halves of O^T
@@ -949,7 +936,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 lsum[r + 1] += hv.y;
               }
             }
-            mbar_wait(bar(P_FREE), (c & 1) ^ 1);  // the previous PV read its P^T
+            // P^T buffer b: its last reader PV(c - 2) completed before QK(c) was issued
             const uint32_t sw = (uint32_t)((ln >> 2) & 1);  // 32B swizzle: 16-byte chunk ^= bit 7 of the address
             const uint32_t a0 = (uint32_t)(ln * 32) + (sw << 4), a1 = (uint32_t)(ln * 32) + ((sw ^ 1u) << 4);
             st_shared_v4(sPn(b, 0) + a0, make_uint4(ph[0], ph[1], ph[2], ph[3]));
@@ -958,14 +945,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               st_shared_v4(sPn(b, 1) + a0, make_uint4(pq[0], pq[1], pq[2], pq[3]));
               st_shared_v4(sPn(b, 1) + a1, make_uint4(pq[4], pq[5], pq[6], pq[7]));
             }
-          } else {
-            mbar_wait(bar(P_FREE), (c & 1) ^ 1);  // see the regular path: one P_FULL phase per tile
           }
           if (vt < kNN && (vt % kN) != 0) zero_v_tail(pl, s0, vt);
           fence_proxy_async_smem();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar(P_FULL));
+          if (lane == 0) mbar_arrive(bar(P_FULL + b));
 #ifdef PAT_TC_TRACE
           if (tr && pl == 0) TC_TRACE(2, 1, c);
 #endif
@@ -990,7 +975,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) sts_f32(xch + (uint32_t)((2 * kNarrow + wq * kNarrow + r) * 4), v);
           }
         }
-        mbar_wait(bar(P_FREE), gl & 1);
+        mbar_wait(bar(P_FREE + (gl & 1)), (gl >> 1) & 1);
 #ifdef PAT_TC_TRACE
         if (tr) ITEM_T(it5);
 #endif
