@@ -630,18 +630,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the A operand of QK, 32 columns at a time -- or into shared memory -- CPT
     // 16-byte chunks of a narrow item's 16-row tile, the 128B-swizzled K-major
     // B operand of S^T = K Q^T
+    // a narrow item's Q chunks of this thread (CPT x 16 B), loaded ahead of the
+    // store: at the start of the previous item's last tile (8 registers)
+    auto load_qn = [&](uint32_t n, uint4* qn) {
+      const int r = ln >> 3;
+      const uint4* src = r < fld(n, kFNrows) ? q_row(n, r) : nullptr;
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) qn[i] = src ? __ldg(src + (ln & 7) * CPT + i) : make_uint4(0, 0, 0, 0);
+    };
+    auto store_qn = [&](const uint4* qn) {
+      const int r = ln >> 3;
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const int ch = (ln & 7) * CPT + i, kb = ch >> 3, cc = ch & 7;
+        st_shared_v4(sQn + (uint32_t)(kb * kNarrow * 128 + r * 128 + ((cc ^ (r & 7)) << 4)), qn[i]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(QT_FULL));
+    };
     auto put_q = [&](uint32_t n) {
       const int nr = fld(n, kFNrows);
       if (is_narrow(n)) {
-        const int r = ln >> 3;
-        const uint4* src = r < nr ? q_row(n, r) : nullptr;
-#pragma unroll
-        for (int i = 0; i < CPT; ++i) {
-          const int ch = (ln & 7) * CPT + i, kb = ch >> 3, cc = ch & 7;
-          const uint4 v = src ? __ldg(src + ch) : make_uint4(0, 0, 0, 0);
-          st_shared_v4(sQn + (uint32_t)(kb * kNarrow * 128 + r * 128 + ((cc ^ (r & 7)) << 4)), v);
-        }
-        fence_proxy_async_smem();
+        uint4 qn[CPT];
+        load_qn(n, qn);
+        store_qn(qn);
+        return;
       } else if (wq * 32 < nr) {
         const uint4* src = ln < nr ? q_row(n, ln) : nullptr;
 #pragma unroll
@@ -855,11 +870,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int r = 0; r < kNarrow; ++r) m_ref[r] = -INFINITY, lsum[r] = 0.f;
         const bool tw = wq < 2;  // warp holds tokens
+        // the next narrow item's Q chunks, loaded at the start of the last tile
+        // and stored once its S^T is consumed (8 registers)
+        uint4 qn[CPT];
+        bool qn_pre = false;
         for (int t = 0; t < ntiles; ++t) {
           const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
           const int s0 = (int)((base + 2u * (uint32_t)t) % kStages);
           const int vt = min(kNN, ntok - t * kNN);  // valid tokens of the tile
-          if (t == ntiles - 1) prefetch_next_q();
+          if (t == ntiles - 1) {
+            prefetch_next_q();
+            qn_pre = have_next && is_narrow(n + 1);
+            if (qn_pre) load_qn(n + 1, qn);
+          }
           mbar_wait(bar(S_FULL + b), (c >> 1) & 1);
 #ifdef PAT_TC_TRACE
           if (tr && t == 0) ITEM_T(it1);
@@ -958,7 +981,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef PAT_TC_TRACE
         if (tr) ITEM_T(it2);
 #endif
-        if (have_next) put_q(n + 1);
+        if (qn_pre) store_qn(qn);
+        else if (have_next) put_q(n + 1);
 #ifdef PAT_TC_TRACE
         if (tr) ITEM_T(it4);
 #endif
