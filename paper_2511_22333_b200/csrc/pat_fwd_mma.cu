@@ -507,11 +507,14 @@ template <int D, typename T>
 __global__ void __launch_bounds__(256) merge_kernel(DevPlan plan, const float* __restrict__ part_o,
                                                     const float* __restrict__ part_lse, T* __restrict__ out) {
   // launched as a programmatic dependent of the forward (launch_merge): the
-  // CTAs are resident when the forward drains; wait for its partials here
+  // CTAs are resident when the forward drains.  The row count and this warp's
+  // first descriptor (plan data) are fetched before waiting for its partials.
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nq = *plan.n_merge;
+  const int4 md0 = gw < nq * plan.H ? __ldg(plan.merge_desc + gw / plan.H) : make_int4(0, 0, 0, 0);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   PAT_SPAN_BEGIN(g_span_mma, 1);
-  merge_rows<D, T>(plan, part_o, part_lse, out, (blockIdx.x * blockDim.x + threadIdx.x) >> 5,
-                   (gridDim.x * blockDim.x) >> 5);
+  merge_rows<D, T>(plan, part_o, part_lse, out, gw, (gridDim.x * blockDim.x) >> 5, nq, md0);
   PAT_SPAN_END(g_span_mma, 1);
 }
 

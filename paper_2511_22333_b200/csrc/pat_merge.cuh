@@ -28,17 +28,18 @@ template <> struct MergeOut<__nv_bfloat16> {
 // Warp `gw` of `nw` folds (query, head) pairs gw, gw + nw, ...  Latency-bound,
 // so lanes fetch up to 32 slot LSEs at once, weights are shuffled, and the
 // weighted O rows are independent loads issued 4 at a time.  Loads bypass L1
-// (ld.global.cg): in the fused phase the partials were written by other CTAs
-// of the same grid.
+// (ld.global.cg): the partials were written by another grid.  The first
+// descriptor (plan data, final before the forward started) and the row count
+// are loaded by the caller before it waits for the forward.
 template <int D, typename T>
 __device__ __forceinline__ void merge_rows(const DevPlan& plan, const float* __restrict__ part_o,
-                                           const float* __restrict__ part_lse, T* __restrict__ out, int gw, int nw) {
+                                           const float* __restrict__ part_lse, T* __restrict__ out, int gw, int nw,
+                                           int nq, int4 md0) {
   const int H = plan.H;
-  const int nq = *plan.n_merge;
   const int lane = threadIdx.x & 31;
   constexpr int PER = D / 32;
   for (int w = gw; w < nq * H; w += nw) {
-    const int4 md = __ldg(plan.merge_desc + w / H);
+    const int4 md = w == gw ? md0 : __ldg(plan.merge_desc + w / H);
     const int q = md.x, head = w % H, base = md.y, n = md.z;
     if (n <= 8) {
       // common case: every slot's LSE and O row are loaded at once (one round
