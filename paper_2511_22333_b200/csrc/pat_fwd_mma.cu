@@ -16,6 +16,8 @@
 // A row whose query is covered by this unit only is normalised and written to
 // the output directly; otherwise (o/l, log2-sum-exp) goes to its fp32 slot and
 // the merge kernel folds the slots (_merge_batch_into, attention.py:187-199).
+#include <atomic>
+#include <algorithm>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 // One warp per (query, head): fold the query's slots with online softmax
 // (_merge_batch_into, attention.py:187-199); see pat_merge.cuh.
 template <int D, typename T>
-__global__ void __launch_bounds__(256) merge_kernel(DevPlan plan, const float* __restrict__ part_o,
+__global__ void __launch_bounds__(256, 3) merge_kernel(DevPlan plan, const float* __restrict__ part_o,
                                                     const float* __restrict__ part_lse, T* __restrict__ out) {
   // launched as a programmatic dependent of the forward (launch_merge): the
   // CTAs are resident when the forward drains.  The row count and this warp's
@@ -572,8 +574,21 @@ static cudaError_t launch_merge_t(const DevPlan& plan, int grid, const float* po
   // programmatic dependent launch: the merge grid is scheduled while the
   // forward drains (its CTAs block in griddepcontrol.wait until the forward
   // grid completed and flushed), hiding the launch gap between the two kernels
+  // a persistent grid: at most the CTAs that are resident at once (warps loop
+  // over rows), so no row waits for a second wave
+  static std::atomic<int> resident[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int cap = dev < 64 ? resident[dev].load(std::memory_order_relaxed) : 0;
+  if (cap == 0) {
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_kernel<D, T>, 256, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = std::max(1, per_sm * sms);
+    if (dev < 64) resident[dev].store(cap, std::memory_order_relaxed);
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3(std::min(grid, cap));
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;

@@ -38,8 +38,12 @@ __device__ __forceinline__ void merge_rows(const DevPlan& plan, const float* __r
   const int H = plan.H;
   const int lane = threadIdx.x & 31;
   constexpr int PER = D / 32;
+  int4 md_next = md0;
   for (int w = gw; w < nq * H; w += nw) {
-    const int4 md = w == gw ? md0 : __ldg(plan.merge_desc + w / H);
+    // this row's descriptor was fetched with the previous row; the next one's
+    // goes out now, so a warp's rows cost one dependent round trip each
+    const int4 md = md_next;
+    if (w + nw < nq * H) md_next = __ldg(plan.merge_desc + (w + nw) / H);
     const int q = md.x, head = w % H, base = md.y, n = md.z;
     if (n <= 8) {
       // common case: every slot's LSE and O row are loaded at once (one round
