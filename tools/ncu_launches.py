@@ -33,11 +33,11 @@ def parse(path):
     return list(kernels.values())
 
 
-def main(path, config, rnd, unique_bytes):
+def main(path, config, rnd, unique_bytes, cmd="bench.py"):
     ks = parse(path)
     out_csv = os.path.join(REPO, "profiles", f"{rnd}_launches_{config}.csv")
     with open(out_csv, "w") as fh:
-        fh.write(f"# {rnd} -- ncu launch list, bench.py {config} (ncu --metrics gpu__time_duration.sum,"
+        fh.write(f"# {rnd} -- ncu launch list, {cmd} {config} (ncu --metrics gpu__time_duration.sum,"
                  "dram__bytes_read.sum,dram__bytes_write.sum,launch__grid_size --clock-control none)\n")
         fh.write("# per-launch times are cold-cache and serialised under ncu: compare SHARES, not absolutes\n")
         fh.write("id,kernel,grid,block,time_ns,dram_read_bytes,dram_write_bytes\n")
@@ -59,7 +59,7 @@ def main(path, config, rnd, unique_bytes):
     res = {
         "workload": config,
         "source": os.path.relpath(out_csv, REPO) + " (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum, "
-                                                   "bench.py layers)",
+                                                   f"{cmd} layers)",
         "layer_dram_bytes": sum(per_kernel.values()),
         "algorithmic_unique_kv_bytes": unique_bytes,
         "per_kernel_dram_bytes": per_kernel,
@@ -71,4 +71,4 @@ def main(path, config, rnd, unique_bytes):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]))
+    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), *sys.argv[5:6])
