@@ -86,6 +86,9 @@ __device__ __forceinline__ long long gtime() {
   } while (0)
 #endif
 
+#ifndef PAT_TRACE_LANE
+#define PAT_TRACE_LANE 0  // item pipeline whose per-tile events tools/tc_trace.py records
+#endif
 constexpr int kThreads = 448;  // per lane: producer, QK issuer, PV issuer; 2 x 4 softmax warps
 constexpr int kCtl = 6;        // control warps
 constexpr int kM = 128;  // rows per item (TMEM lanes)
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // of the stage was one: same parity as KV_EMPTY)
           if (gt >= (uint32_t)kStages && gt - kStages < pair_upto)
             mbar_wait(bar(XKV_EMPTY + s), ((gt / kStages) & 1) ^ 1);
-          if (pl == 0) TC_TRACE(0, 0, gt);
+          if (pl == PAT_TRACE_LANE) TC_TRACE(0, 0, gt);
           if (elect_one()) mbar_expect_tx(bar(KV_FULL + s), (uint32_t)(ngrp * KB * 2048 * 2));
           __syncwarp();
           for (int gr = 0; gr < ngrp; ++gr) {
@@ -519,16 +522,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t c = tcnt + (uint32_t)t;
             const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
             const int s = (int)(g % kStages);
-            if (pl == 0) TC_TRACE(1, 2, c);
+            if (pl == PAT_TRACE_LANE) TC_TRACE(1, 2, c);
             mbar_wait(barL(src, KV_FULL + s), (g / kStages) & 1);
             if (narrow && ntok - t * kNN > kN) mbar_wait(barL(src, KV_FULL + s + 1), ((g + 1) / kStages) & 1);
-            if (pl == 0) TC_TRACE(1, 3, c);
+            if (pl == PAT_TRACE_LANE) TC_TRACE(1, 3, c);
             // buffer c & 1 was last read by PV(c - 2)
             mbar_wait(bar(P_FREE + (c & 1)), ((c >> 1) & 1) ^ 1);
             if (t == 0) mbar_wait(bar(QT_FULL), qu++ & 1);
             const uint32_t sbuf = tg + 32u * (c & 1);
             tc_fence_after();
-            if (pl == 0) TC_TRACE(1, 0, c);
+            if (pl == PAT_TRACE_LANE) TC_TRACE(1, 0, c);
             if (elect_one()) {
               if (narrow) {
 #pragma unroll
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
             const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
             const int s = (int)(g % kStages);
-            if (pl == 0) TC_TRACE(1, 4, c);
+            if (pl == PAT_TRACE_LANE) TC_TRACE(1, 4, c);
             mbar_wait(bar(P_FULL + b), (c >> 1) & 1);
             if (t == 0) mbar_wait(bar(O_EMPTY), (ou & 1) ^ 1);
             tc_fence_after();
@@ -596,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             __syncwarp();
-            if (pl == 0) TC_TRACE(1, 1, c);
+            if (pl == PAT_TRACE_LANE) TC_TRACE(1, 1, c);
           }
           ++ou;
           if (src == pl) rpos = base + (uint32_t)((ntok + kN - 1) / kN);
@@ -729,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(bar(S_FULL + (c & 1)), (c >> 1) & 1);
 #ifdef PAT_TC_TRACE
           if (tr && t == 0) ITEM_T(it1);
-          if (tr && pl == 0) TC_TRACE(2, 0, c);
+          if (tr && pl == PAT_TRACE_LANE) TC_TRACE(2, 0, c);
 #endif
           tc_fence_after();
           if (wlive) {
@@ -805,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(bar(P_FULL + (c & 1)));
 #ifdef PAT_TC_TRACE
-          if (tr && pl == 0) TC_TRACE(2, 1, c);
+          if (tr && pl == PAT_TRACE_LANE) TC_TRACE(2, 1, c);
 #endif
         }
 #ifdef PAT_TC_TRACE
@@ -886,7 +889,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(bar(S_FULL + b), (c >> 1) & 1);
 #ifdef PAT_TC_TRACE
           if (tr && t == 0) ITEM_T(it1);
-          if (tr && pl == 0) TC_TRACE(2, 0, c);
+          if (tr && pl == PAT_TRACE_LANE) TC_TRACE(2, 0, c);
 #endif
           tc_fence_after();
           float x[kNarrow];
@@ -975,7 +978,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(bar(P_FULL + b));
 #ifdef PAT_TC_TRACE
-          if (tr && pl == 0) TC_TRACE(2, 1, c);
+          if (tr && pl == PAT_TRACE_LANE) TC_TRACE(2, 1, c);
 #endif
         }
 #ifdef PAT_TC_TRACE
