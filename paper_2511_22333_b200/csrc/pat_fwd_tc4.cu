@@ -100,8 +100,12 @@ constexpr int kStages = PAT_TC4_STAGES;  // per lane
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kNarrow = 16;                // items of <= 16 rows run transposed (N = 16)
-constexpr int kNN = 2 * kN;                // tokens per narrow tile (a stage pair)
-static_assert(kStages % 2 == 0, "narrow tiles are aligned stage pairs");
+#ifndef PAT_TC4_NSTG
+#define PAT_TC4_NSTG 2
+#endif
+constexpr int kNStg = PAT_TC4_NSTG;        // ring stages per narrow tile (1 or 2)
+constexpr int kNN = kNStg * kN;            // tokens per narrow tile
+static_assert((kNStg == 1 || kNStg == 2) && kStages % kNStg == 0, "narrow tiles are aligned stage groups");
 
 struct ItemSlot {
   int32_t idx;
@@ -428,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // first ring position of the item: narrow items start on an even stage
         // (their 64-token tiles are stage pairs); the odd one is skipped
         const bool narrow = it >= 0 && !shared && item.nrows <= kNarrow;
-        if (!shared) g0 = narrow ? ((gt + 1) & ~1u) : gt;
+        if (!shared) g0 = narrow ? ((gt + kNStg - 1) & ~(uint32_t)(kNStg - 1)) : gt;
         if (lane == 0) {
           ring[slot].idx = it;
           ring[slot].pad[0] = shared;
@@ -520,11 +524,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (is_qk) {
           for (int t = 0; t < ntiles; ++t) {
             const uint32_t c = tcnt + (uint32_t)t;
-            const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
+            const uint32_t g = narrow ? base + (uint32_t)(kNStg * t) : base + (uint32_t)t;
             const int s = (int)(g % kStages);
             if (pl == PAT_TRACE_LANE) TC_TRACE(1, 2, c);
             mbar_wait(barL(src, KV_FULL + s), (g / kStages) & 1);
-            if (narrow && ntok - t * kNN > kN) mbar_wait(barL(src, KV_FULL + s + 1), ((g + 1) / kStages) & 1);
+            if (kNStg == 2 && narrow && ntok - t * kNN > kN)
+              mbar_wait(barL(src, KV_FULL + s + 1), ((g + 1) / kStages) & 1);
             if (pl == PAT_TRACE_LANE) TC_TRACE(1, 3, c);
             // buffer c & 1 was last read by PV(c - 2)
             mbar_wait(bar(P_FREE + (c & 1)), ((c >> 1) & 1) ^ 1);
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           for (int t = 0; t < ntiles; ++t) {
             const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
-            const uint32_t g = narrow ? base + 2u * (uint32_t)t : base + (uint32_t)t;
+            const uint32_t g = narrow ? base + (uint32_t)(kNStg * t) : base + (uint32_t)t;
             const int s = (int)(g % kStages);
             if (pl == PAT_TRACE_LANE) TC_TRACE(1, 4, c);
             mbar_wait(bar(P_FULL + b), (c >> 1) & 1);
@@ -879,7 +884,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool qn_pre = false;
         for (int t = 0; t < ntiles; ++t) {
           const uint32_t c = tcnt + (uint32_t)t, b = c & 1;
-          const int s0 = (int)((base + 2u * (uint32_t)t) % kStages);
+          const int s0 = (int)((base + (uint32_t)(kNStg * t)) % kStages);
           const int vt = min(kNN, ntok - t * kNN);  // valid tokens of the tile
           if (t == ntiles - 1) {
             prefetch_next_q();
