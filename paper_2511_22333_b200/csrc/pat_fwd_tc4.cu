@@ -7,17 +7,18 @@
 // ring, so one lane's item boundary (Q load, last PV, O read-out and stores)
 // overlaps the other lane's tiles instead of stalling the SM:
 //
-//   warp 0 / 2   producer of lane 0 / 1: claims items, resolves per-row (query
+//   warps 0 / 3  producer of lane 0 / 1: claims items, resolves per-row (query
 //                id, partial slot) into a 2-slot item ring, warms L2 with the
 //                item's Q rows, issues TMA boxes of 16-token page slices of K
 //                and V (32-token stages, 128B swizzle) straight from the paged
 //                vLLM cache;
-//   warp 1 / 3   MMA issuer of lane 0 / 1 (warp 1 also allocates TMEM):
+//   warps 1 / 4  QK issuer of lane 0 / 1 (warp 1 also allocates TMEM):
 //                  S[b] = Q K^T   (TS: Q from TMEM, K from smem, M=128 N=32)
+//   warps 2 / 5  PV issuer of lane 0 / 1:
 //                  O   += P[b] V  (TS: P from TMEM over S[b], V from smem)
-//                with S/P double-buffered (b = tile & 1): QK of tile t+1 runs
-//                while the softmax works on tile t;
-//   warps 4-7    softmax / epilogue of lane 0, warps 8-11 of lane 1: one thread
+//                S/P are double-buffered (b = tile & 1): QK(t) waits only for
+//                PV(t-2), so it runs a tile ahead of the softmax;
+//   warps 6-9    softmax / epilogue of lane 0, warps 10-13 of lane 1: one thread
 //                per TMEM lane = one row of the item (query x GQA head), the
 //                whole 32-column tile per thread, so a row's running max, sum
 //                and O never leave its thread: no cross-warp fold, no CTA-wide
