@@ -17,9 +17,12 @@
 namespace pat {
 
 // Measured on B200 for the two-lane tcgen05 kernel (tools/item_log.py: ~0.72 us
-// per 32-token tile per lane with every SM streaming, ~1.2 us + ~2 us per 128
-// rows of item boundary); see DESIGN.md §4.
-static pat_cost_model g_cost_model = {1200.0, 2000.0, 1440.0, 1500.0, 6.5e3};
+// per 32-token tile per lane with every SM streaming; an item boundary -- start
+// latency + epilogue -- of ~3-4 us for a narrow item and ~6 us for a 128-row
+// one), the per-item constant chosen by tools/cm_sweep.py over c1-c5 (3.6 us:
+// c4 keeps its 8k root unsplit, 196.6 -> 184.3 us; c1-c3, c5 unchanged); see
+// DESIGN.md §7.
+static pat_cost_model g_cost_model = {3600.0, 2000.0, 1440.0, 1500.0, 6.5e3};
 constexpr int kTcLanesPerSm = 2;  // independent item pipelines per tcgen05 CTA
 static std::mutex g_cost_mu;
 

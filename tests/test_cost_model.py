@@ -36,7 +36,7 @@ def _units(name):
 def test_default_model_is_the_measured_two_lane_constants():
     m = CAL.get_cost_model()
     assert (m.tc_item_ns, m.tc_item_row_ns, m.tc_step_ns, m.stream_item_ns, m.hbm_bytes_per_ns) == \
-        (1200.0, 2000.0, 1440.0, 1500.0, 6500.0)
+        (3600.0, 2000.0, 1440.0, 1500.0, 6500.0)
 
 
 def test_set_get_roundtrip_and_validation(restore_model):
